@@ -1,0 +1,186 @@
+/*
+ * g2m.h -- C ABI of libg2m.so, the B200 (sm_100a) pattern-mining engine.
+ *
+ * This is the drop-in boundary behind the reference package's execution
+ * operators.  Every entry point uses plain pointers and fixed-width integers
+ * (no torch / numpy / C++ types), returns a status code and leaves a
+ * thread-local message in g2m_last_error() on failure.
+ *
+ * Reference interfaces replaced (paths relative to the reference package
+ * pkg/src/patminer/):
+ *
+ *   g2m_graph_create        Graph(row_offsets, neighbors, labels, oriented)
+ *                            graph.py:38-61 -- host CSR (u64 offsets,
+ *                            u32 ids) becomes a device-resident replica.
+ *   g2m_graph_from_edges    from_edges(edges, num_vertices, labels)
+ *                            graph.py:116-142 -- drop self loops,
+ *                            symmetrise, dedup, CSR, on the device.
+ *   g2m_graph_orient        orient(g) graph.py:204-221 -- keep u->v iff
+ *                            (deg_u,u) < (deg_v,v), on the device.
+ *   g2m_graph_download      host view of a device graph (Graph arrays).
+ *   g2m_kernel_compile      the "codegen" step: the CUDA source emitted for
+ *                            one PlanForest (plan.py:205-301; analog of
+ *                            emit_source plan.py:334-347) is compiled with
+ *                            NVRTC for sm_100a.
+ *   g2m_run                 run_dfs(g, forest, tasks, cfg, sink=None)
+ *                            executor.py:339-408 (count terminals) and
+ *                            run_dfs_lgs executor.py:526-599; one call per
+ *                            device -- scheduler.run_on_devices
+ *                            (scheduler.py:207-239) issues one per GPU.
+ *   g2m_list                run_dfs(..., sink) list mode: matches are
+ *                            produced on the device in exact reference
+ *                            order (task order, then DFS order) and handed
+ *                            to the host in batches (executor.py:275-280).
+ *   g2m_setop_batch         setops.intersect/intersect_count/difference/
+ *                            difference_count (setops.py:35-84) as a
+ *                            batched device call (kernel-library parity).
+ *
+ * Status codes map onto the reference's exceptions:
+ *   G2M_OK 0, G2M_EUSAGE 1 -> ValueError, G2M_EBUDGET 2 -> BudgetError,
+ *   G2M_ECUDA 3 -> RuntimeError, G2M_STOPPED 4 -> RunResult.stopped_early.
+ */
+#ifndef G2M_H
+#define G2M_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define G2M_ABI_VERSION 1
+
+#define G2M_OK 0
+#define G2M_EUSAGE 1
+#define G2M_EBUDGET 2
+#define G2M_ECUDA 3
+#define G2M_STOPPED 4
+
+/* Task kinds (executor.py:284-325). */
+#define G2M_TASKS_EDGE 0
+#define G2M_TASKS_VERTEX 1
+
+/* Task sources. IMPLICIT: the default task list of run_dfs/run_job
+ * (graph.py:270-286 all_edge_tasks / reduced src>dst, or arange(|V|)),
+ * generated on the device in the reference's order.  PAIRS: an explicit
+ * EdgeTaskList.edges int64 (m,2) array.  VERTICES: explicit int64 vertex
+ * ids.  INDEX: int64 indices into the IMPLICIT list (Schedule queues,
+ * scheduler.py:27-105). */
+#define G2M_SRC_IMPLICIT 0
+#define G2M_SRC_PAIRS 1
+#define G2M_SRC_VERTICES 2
+#define G2M_SRC_INDEX 3
+
+typedef struct g2m_graph g2m_graph;
+typedef struct g2m_kernel g2m_kernel;
+
+typedef struct g2m_graph_info {
+    uint64_t num_vertices;
+    uint64_t num_slots;     /* directed CSR entries == Graph.num_edges */
+    uint64_t max_degree;    /* Graph.max_degree (out-degree if oriented) */
+    int32_t oriented;
+    int32_t labeled;
+    int32_t device;
+    int32_t reserved;
+} g2m_graph_info;
+
+typedef struct g2m_task_spec {
+    int32_t kind;           /* G2M_TASKS_EDGE / G2M_TASKS_VERTEX */
+    int32_t source;         /* G2M_SRC_* */
+    int32_t reduced;        /* IMPLICIT/INDEX edge lists: only src > dst */
+    int32_t reserved;
+    const int64_t* data;    /* host array for PAIRS (2*count) / VERTICES / INDEX */
+    uint64_t count;         /* entries in data (ignored for IMPLICIT) */
+    uint64_t rr_chunk;      /* IMPLICIT only: 0 = whole list, else chunked
+                               round-robin partition (scheduler.py:77-94) */
+    uint32_t rr_parts;
+    uint32_t rr_part;
+} g2m_task_spec;
+
+typedef struct g2m_kernel_meta {
+    int32_t num_patterns;   /* counters, in forest.pattern_ids order */
+    int32_t num_slots;      /* materialised-set slots per warp */
+    int32_t granularity;    /* G2M_TASKS_EDGE / G2M_TASKS_VERTEX */
+    int32_t max_level;      /* deepest plan level */
+    int32_t needs_labels;
+    int32_t list_mode;      /* kernel emits matches */
+    int32_t smem_slot_cap;  /* >0: slots live in shared memory with this
+                               many u32 entries each; 0: global scratch */
+    int32_t warps_per_block;
+    int32_t instrumented;   /* kernel accumulates algorithmic bytes */
+    int32_t warp_words;     /* dynamic shared memory per warp (u32 words) */
+    int32_t reserved[6];
+} g2m_kernel_meta;
+
+typedef struct g2m_run_config {
+    int32_t blocks;         /* 0 = SM count x occupancy */
+    int32_t reserved0;
+    uint64_t chunk;         /* tasks per dynamic work grab, 0 = auto */
+    uint64_t scratch_budget;/* bytes for per-warp global slots, 0 = auto */
+    int32_t time_kernel;    /* record kernel time with CUDA events */
+    int32_t reserved[5];
+} g2m_run_config;
+
+typedef struct g2m_run_stats {
+    uint64_t tasks;             /* tasks in the list handed to the kernel */
+    uint64_t tasks_active;      /* tasks passing the level-2 filter */
+    uint64_t warps;             /* resident warps launched */
+    uint64_t alg_bytes_lo;      /* SURVEY 8(d) algorithmic bytes (instrumented kernels) */
+    uint64_t alg_bytes_hi;
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint64_t high_water[8];     /* max materialised size per slot */
+    double kernel_ms;           /* CUDA-event time of the mining kernel */
+    double total_ms;            /* wall time of the whole call */
+} g2m_run_stats;
+
+/* Match callback for g2m_list: `n` tuples of `k` vertex ids (level order),
+ * all for pattern index `pid`. Return nonzero to stop (sink -> True). */
+typedef int (*g2m_match_cb)(void* user, int32_t pid, int32_t k, uint64_t n,
+                            const uint32_t* tuples);
+
+const char* g2m_last_error(void);
+int32_t g2m_abi_version(void);
+int g2m_device_count(int32_t* out);
+
+int g2m_graph_create(int32_t device, const uint64_t* row_offsets, uint64_t num_vertices,
+                     const uint32_t* neighbors, uint64_t num_slots,
+                     const uint32_t* labels_or_null, int32_t oriented, g2m_graph** out);
+int g2m_graph_from_edges(int32_t device, const int64_t* edges, uint64_t num_pairs,
+                         uint64_t num_vertices, const uint32_t* labels_or_null,
+                         g2m_graph** out);
+int g2m_graph_orient(const g2m_graph* g, g2m_graph** out);
+int g2m_graph_replicate(const g2m_graph* g, int32_t device, g2m_graph** out);
+int g2m_graph_info_get(const g2m_graph* g, g2m_graph_info* info);
+int g2m_graph_download(const g2m_graph* g, uint64_t* row_offsets, uint32_t* neighbors,
+                       uint32_t* labels_or_null);
+int g2m_graph_destroy(g2m_graph* g);
+
+int g2m_kernel_compile(const char* cuda_source, const char* kernel_name,
+                       const char* const* header_sources, const char* const* header_names,
+                       int32_t num_headers, const g2m_kernel_meta* meta, g2m_kernel** out);
+int g2m_kernel_get_meta(const g2m_kernel* k, g2m_kernel_meta* meta);
+int g2m_kernel_destroy(g2m_kernel* k);
+
+int g2m_run(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* tasks,
+            const g2m_run_config* cfg, uint64_t* counts_lo_hi, g2m_run_stats* stats);
+int g2m_list(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* tasks,
+             const g2m_run_config* cfg, g2m_match_cb cb, void* user,
+             uint64_t* counts_lo_hi, g2m_run_stats* stats);
+
+/* Batched sorted-set kernels (setops.py:35-84). Lists are concatenated u32
+ * arrays addressed by u64 offsets; op: 0 intersect, 1 intersect_count,
+ * 2 difference, 3 difference_count. bound[i] < 0 means "no bound".
+ * Outputs: out_count[i]; for materialising ops the elements at
+ * out_values[out_offsets[i] ...] (out_offsets sized by |a|). */
+int g2m_setop_batch(int32_t device, int32_t op, uint64_t num_cases,
+                    const uint32_t* a_values, const uint64_t* a_offsets,
+                    const uint32_t* b_values, const uint64_t* b_offsets,
+                    const int64_t* bounds, uint64_t* out_count, uint32_t* out_values);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* G2M_H */

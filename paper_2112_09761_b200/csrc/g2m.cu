@@ -1,0 +1,983 @@
+// g2m.cu -- libg2m.so: C ABI (include/g2m.h) of the B200 pattern-mining engine.
+//
+// Owns device graphs (CSR replicas), the NVRTC compiler for generated plan
+// kernels, task-list preparation, kernel launch and result collection.
+// Fixed (non-generated) kernels live here too: orientation, reduced-task
+// offsets, CSR construction, task conversion, batched set operations.
+#include "g2m.h"
+#include "g2m_device.cuh"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define G2M_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(G2M_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Driver API entry points, resolved through the runtime so the library
+// loads on hosts without libcuda.so (the build container) and binds to the
+// driver only when a GPU is actually used.
+struct Drv {
+    CUresult (*ModuleLoadData)(CUmodule*, const void*);
+    CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*);
+    CUresult (*ModuleUnload)(CUmodule);
+    CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
+    CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t);
+    CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             unsigned, CUstream, void**, void**);
+    CUresult (*GetErrorString)(CUresult, const char**);
+    bool ok = false;
+};
+static Drv g_drv;
+static std::mutex g_drv_mu;
+
+static int drv_init() {
+    std::lock_guard<std::mutex> lk(g_drv_mu);
+    if (g_drv.ok) return 0;
+    struct { const char* name; void** slot; } tab[] = {
+        {"cuModuleLoadData", (void**)&g_drv.ModuleLoadData},
+        {"cuModuleGetFunction", (void**)&g_drv.ModuleGetFunction},
+        {"cuModuleUnload", (void**)&g_drv.ModuleUnload},
+        {"cuFuncSetAttribute", (void**)&g_drv.FuncSetAttribute},
+        {"cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&g_drv.OccupancyMaxActiveBlocksPerMultiprocessor},
+        {"cuLaunchKernel", (void**)&g_drv.LaunchKernel},
+        {"cuGetErrorString", (void**)&g_drv.GetErrorString},
+    };
+    for (auto& t : tab) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint(t.name, t.slot, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !*t.slot)
+            return -1;
+    }
+    g_drv.ok = true;
+    return 0;
+}
+
+#define G2M_CU(call)                                                                    \
+    do {                                                                                \
+        if (drv_init()) return fail(G2M_ECUDA, "CUDA driver entry points unavailable"); \
+        CUresult r_ = g_drv.call;                                                       \
+        if (r_ != CUDA_SUCCESS) {                                                       \
+            const char* s_ = nullptr;                                                   \
+            g_drv.GetErrorString(r_, &s_);                                              \
+            return fail(G2M_ECUDA, std::string(#call) + ": " + (s_ ? s_ : "?"));        \
+        }                                                                               \
+    } while (0)
+
+#define G2M_TRY(call)               \
+    do {                            \
+        int rc_ = (call);           \
+        if (rc_ != G2M_OK) return rc_; \
+    } while (0)
+
+using Clock = std::chrono::steady_clock;
+
+static double ms_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// ---------------------------------------------------------------------------
+// device buffers
+// ---------------------------------------------------------------------------
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    int ensure(size_t n) {
+        if (n <= bytes && p) return G2M_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (n == 0) n = 16;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(G2M_ECUDA, std::string("cudaMalloc(") + std::to_string(n) +
+                                       "): " + cudaGetErrorString(e));
+        }
+        bytes = n;
+        return G2M_OK;
+    }
+    template <typename T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// Per-device reusable workspace (one run at a time per device).
+struct DevState {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    DevBuf counters;    // next, counts, stats
+    DevBuf scratch;     // per-warp slots
+    DevBuf tasks_a, tasks_b, task_match, matches, cub_tmp;
+    int sms = 0;
+};
+
+static std::mutex g_dev_mu;
+static std::map<int, std::unique_ptr<DevState>> g_devs;
+
+static int dev_state(int dev, DevState** out) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_devs.find(dev);
+    if (it == g_devs.end()) {
+        G2M_CUDA(cudaSetDevice(dev));
+        G2M_CUDA(cudaFree(0));
+        auto st = std::make_unique<DevState>();
+        G2M_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+        G2M_CUDA(cudaEventCreate(&st->ev0));
+        G2M_CUDA(cudaEventCreate(&st->ev1));
+        G2M_CUDA(cudaDeviceGetAttribute(&st->sms, cudaDevAttrMultiProcessorCount, dev));
+        it = g_devs.emplace(dev, std::move(st)).first;
+    }
+    *out = it->second.get();
+    return G2M_OK;
+}
+
+// ---------------------------------------------------------------------------
+// graph
+// ---------------------------------------------------------------------------
+
+struct g2m_graph {
+    int dev = 0;
+    uint64_t nv = 0, slots = 0, maxdeg = 0;
+    int oriented = 0;
+    DevBuf off, nbr, labels;
+    std::mutex mu;
+    DevBuf red_off;          // reduced (src > dst) task offsets, lazily built
+    uint64_t red_total = 0;
+    bool has_red = false;
+};
+
+__global__ void k_max_degree(const u64* off, u64 nv, u64* out) {
+    u64 best = 0;
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x)
+        best = max(best, off[v + 1] - off[v]);
+    for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(G2M_FULL, best, o));
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
+static int grid_for(DevState* st, uint64_t n, int threads) {
+    uint64_t want = (n + threads - 1) / threads;
+    uint64_t cap = (uint64_t)st->sms * 16;
+    if (want > cap) want = cap;
+    if (want < 1) want = 1;
+    return (int)want;
+}
+
+static int finish_graph(g2m_graph* g, DevState* st) {
+    DevBuf tmp;
+    G2M_TRY(tmp.ensure(8));
+    G2M_CUDA(cudaMemsetAsync(tmp.p, 0, 8, st->stream));
+    if (g->nv) {
+        k_max_degree<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, tmp.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_CUDA(cudaMemcpyAsync(&g->maxdeg, tmp.p, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return G2M_OK;
+}
+
+extern "C" const char* g2m_last_error(void) { return g_err.c_str(); }
+extern "C" int32_t g2m_abi_version(void) { return G2M_ABI_VERSION; }
+
+extern "C" int g2m_device_count(int32_t* out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = 0;
+        return fail(G2M_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *out = n;
+    return G2M_OK;
+}
+
+extern "C" int g2m_graph_create(int32_t device, const uint64_t* row_offsets, uint64_t num_vertices,
+                                const uint32_t* neighbors, uint64_t num_slots,
+                                const uint32_t* labels, int32_t oriented, g2m_graph** out) {
+    if (!out) return fail(G2M_EUSAGE, "null output handle");
+    if (!row_offsets && num_vertices) return fail(G2M_EUSAGE, "null row_offsets");
+    DevState* st;
+    G2M_TRY(dev_state(device, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(device));
+    auto g = std::make_unique<g2m_graph>();
+    g->dev = device;
+    g->nv = num_vertices;
+    g->slots = num_slots;
+    g->oriented = oriented ? 1 : 0;
+    G2M_TRY(g->off.ensure((num_vertices + 1) * 8));
+    G2M_TRY(g->nbr.ensure(std::max<uint64_t>(num_slots, 1) * 4));
+    if (row_offsets)
+        G2M_CUDA(cudaMemcpyAsync(g->off.p, row_offsets, (num_vertices + 1) * 8, cudaMemcpyHostToDevice, st->stream));
+    else
+        G2M_CUDA(cudaMemsetAsync(g->off.p, 0, 8, st->stream));
+    if (num_slots)
+        G2M_CUDA(cudaMemcpyAsync(g->nbr.p, neighbors, num_slots * 4, cudaMemcpyHostToDevice, st->stream));
+    if (labels) {
+        G2M_TRY(g->labels.ensure(std::max<uint64_t>(num_vertices, 1) * 4));
+        if (num_vertices)
+            G2M_CUDA(cudaMemcpyAsync(g->labels.p, labels, num_vertices * 4, cudaMemcpyHostToDevice, st->stream));
+    }
+    G2M_TRY(finish_graph(g.get(), st));
+    *out = g.release();
+    return G2M_OK;
+}
+
+extern "C" int g2m_graph_info_get(const g2m_graph* g, g2m_graph_info* info) {
+    if (!g || !info) return fail(G2M_EUSAGE, "null argument");
+    info->num_vertices = g->nv;
+    info->num_slots = g->slots;
+    info->max_degree = g->maxdeg;
+    info->oriented = g->oriented;
+    info->labeled = g->labels.p ? 1 : 0;
+    info->device = g->dev;
+    info->reserved = 0;
+    return G2M_OK;
+}
+
+extern "C" int g2m_graph_download(const g2m_graph* g, uint64_t* row_offsets, uint32_t* neighbors,
+                                  uint32_t* labels) {
+    if (!g) return fail(G2M_EUSAGE, "null graph");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    if (row_offsets)
+        G2M_CUDA(cudaMemcpyAsync(row_offsets, g->off.p, (g->nv + 1) * 8, cudaMemcpyDeviceToHost, st->stream));
+    if (neighbors && g->slots)
+        G2M_CUDA(cudaMemcpyAsync(neighbors, g->nbr.p, g->slots * 4, cudaMemcpyDeviceToHost, st->stream));
+    if (labels && g->labels.p && g->nv)
+        G2M_CUDA(cudaMemcpyAsync(labels, g->labels.p, g->nv * 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return G2M_OK;
+}
+
+extern "C" int g2m_graph_destroy(g2m_graph* g) {
+    if (!g) return G2M_OK;
+    cudaSetDevice(g->dev);
+    delete g;
+    return G2M_OK;
+}
+
+// ---- orientation (graph.py:204-221): keep u->w iff (deg u, u) < (deg w, w)
+
+__device__ __forceinline__ bool orient_keep(const u64* off, u32 u, u32 w) {
+    u64 du = off[u + 1] - off[u], dw = __ldg(off + w + 1) - __ldg(off + w);
+    return du < dw || (du == dw && u < w);
+}
+
+__global__ void k_orient_count(const u64* off, const u32* nbr, u64 nv, u64* cnt) {
+    const u32 lane = g2m_lane();
+    for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
+         u += ((u64)gridDim.x * blockDim.x) >> 5) {
+        u64 b = off[u], e = off[u + 1];
+        u32 c = 0;
+        for (u64 base = b; base < e; base += 32) {
+            u64 i = base + lane;
+            bool k = i < e && orient_keep(off, (u32)u, __ldg(nbr + i));
+            c += __popc(__ballot_sync(G2M_FULL, k));
+        }
+        if (lane == 0) cnt[u] = c;
+    }
+}
+
+__global__ void k_orient_fill(const u64* off, const u32* nbr, u64 nv, const u64* noff, u32* out) {
+    const u32 lane = g2m_lane();
+    for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
+         u += ((u64)gridDim.x * blockDim.x) >> 5) {
+        u64 b = off[u], e = off[u + 1];
+        u64 w = noff[u];
+        for (u64 base = b; base < e; base += 32) {
+            u64 i = base + lane;
+            u32 x = i < e ? __ldg(nbr + i) : 0u;
+            bool k = i < e && orient_keep(off, (u32)u, x);
+            u32 m = __ballot_sync(G2M_FULL, k);
+            if (k) out[w + __popc(m & g2m_lanemask_lt())] = x;
+            w += __popc(m);
+        }
+    }
+}
+
+static int exclusive_scan_u64(DevState* st, const u64* in, u64* out, uint64_t n) {
+    // out has n+1 entries; out[0] = 0, out[i+1] = sum in[0..i]
+    G2M_CUDA(cudaMemsetAsync(out, 0, 8, st->stream));
+    if (n == 0) return G2M_OK;
+    size_t tmp = 0;
+    G2M_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out + 1, (int64_t)n, st->stream));
+    G2M_TRY(st->cub_tmp.ensure(tmp));
+    G2M_CUDA(cub::DeviceScan::InclusiveSum(st->cub_tmp.p, tmp, in, out + 1, (int64_t)n, st->stream));
+    return G2M_OK;
+}
+
+extern "C" int g2m_graph_orient(const g2m_graph* g, g2m_graph** out) {
+    if (!g || !out) return fail(G2M_EUSAGE, "null argument");
+    if (g->oriented) return fail(G2M_EUSAGE, "graph is already oriented");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    auto o = std::make_unique<g2m_graph>();
+    o->dev = g->dev;
+    o->nv = g->nv;
+    o->oriented = 1;
+    G2M_TRY(o->off.ensure((g->nv + 1) * 8));
+    DevBuf cnt;
+    G2M_TRY(cnt.ensure(std::max<uint64_t>(g->nv, 1) * 8));
+    if (g->nv) {
+        int grid = grid_for(st, g->nv * 32, 256);
+        k_orient_count<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), g->nv, cnt.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), o->off.as<u64>(), g->nv));
+    G2M_CUDA(cudaMemcpyAsync(&o->slots, o->off.as<u64>() + g->nv, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    G2M_TRY(o->nbr.ensure(std::max<uint64_t>(o->slots, 1) * 4));
+    if (g->nv) {
+        int grid = grid_for(st, g->nv * 32, 256);
+        k_orient_fill<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), g->nv,
+                                                     o->off.as<u64>(), o->nbr.as<u32>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    if (g->labels.p) {
+        G2M_TRY(o->labels.ensure(std::max<uint64_t>(g->nv, 1) * 4));
+        G2M_CUDA(cudaMemcpyAsync(o->labels.p, g->labels.p, g->nv * 4, cudaMemcpyDeviceToDevice, st->stream));
+    }
+    G2M_TRY(finish_graph(o.get(), st));
+    *out = o.release();
+    return G2M_OK;
+}
+
+extern "C" int g2m_graph_replicate(const g2m_graph* g, int32_t device, g2m_graph** out) {
+    if (!g || !out) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(device, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(device));
+    auto o = std::make_unique<g2m_graph>();
+    o->dev = device;
+    o->nv = g->nv;
+    o->slots = g->slots;
+    o->maxdeg = g->maxdeg;
+    o->oriented = g->oriented;
+    G2M_TRY(o->off.ensure((g->nv + 1) * 8));
+    G2M_TRY(o->nbr.ensure(std::max<uint64_t>(g->slots, 1) * 4));
+    // peer copy over NVLink (staged through the host when peers are not accessible)
+    G2M_CUDA(cudaMemcpyPeerAsync(o->off.p, device, g->off.p, g->dev, (g->nv + 1) * 8, st->stream));
+    if (g->slots)
+        G2M_CUDA(cudaMemcpyPeerAsync(o->nbr.p, device, g->nbr.p, g->dev, g->slots * 4, st->stream));
+    if (g->labels.p) {
+        G2M_TRY(o->labels.ensure(std::max<uint64_t>(g->nv, 1) * 4));
+        G2M_CUDA(cudaMemcpyPeerAsync(o->labels.p, device, g->labels.p, g->dev, g->nv * 4, st->stream));
+    }
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    *out = o.release();
+    return G2M_OK;
+}
+
+// ---- CSR construction on the device (graph.py:116-142)
+
+__global__ void k_edge_keys(const i64* edges, u64 m, u64 n, u64* keys, u64* nkeys) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+        u64 u = (u64)edges[2 * i], v = (u64)edges[2 * i + 1];
+        if (u != v) {
+            u64 slot = atomicAdd(nkeys, 2ull);
+            keys[slot] = u * n + v;
+            keys[slot + 1] = v * n + u;
+        }
+    }
+}
+
+__global__ void k_keys_to_csr(const u64* keys, u64 nk, u64 n, u32* nbr, u64* cnt) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nk; i += (u64)gridDim.x * blockDim.x) {
+        u64 k = keys[i];
+        u64 s = k / n;
+        nbr[i] = (u32)(k - s * n);
+        atomicAdd(cnt + s, 1ull);
+    }
+}
+
+extern "C" int g2m_graph_from_edges(int32_t device, const int64_t* edges, uint64_t m,
+                                    uint64_t num_vertices, const uint32_t* labels, g2m_graph** out) {
+    if (!out) return fail(G2M_EUSAGE, "null output handle");
+    if (2 * m > (uint64_t)INT32_MAX) return fail(G2M_EUSAGE, "edge list too large for one device sort");
+    DevState* st;
+    G2M_TRY(dev_state(device, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(device));
+    const uint64_t n = num_vertices;
+    DevBuf din, keys, keys2, nk, cnt;
+    G2M_TRY(din.ensure(std::max<uint64_t>(m, 1) * 16));
+    G2M_TRY(keys.ensure(std::max<uint64_t>(2 * m, 1) * 8));
+    G2M_TRY(keys2.ensure(std::max<uint64_t>(2 * m, 1) * 8));
+    G2M_TRY(nk.ensure(16));
+    G2M_TRY(cnt.ensure(std::max<uint64_t>(n, 1) * 8));
+    G2M_CUDA(cudaMemsetAsync(nk.p, 0, 16, st->stream));
+    G2M_CUDA(cudaMemsetAsync(cnt.p, 0, std::max<uint64_t>(n, 1) * 8, st->stream));
+    if (m) {
+        G2M_CUDA(cudaMemcpyAsync(din.p, edges, m * 16, cudaMemcpyHostToDevice, st->stream));
+        k_edge_keys<<<grid_for(st, m, 256), 256, 0, st->stream>>>(din.as<i64>(), m, n, keys.as<u64>(), nk.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    uint64_t nkeys = 0;
+    G2M_CUDA(cudaMemcpyAsync(&nkeys, nk.p, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    int nbits = 0;
+    while (nbits < 33 && (n >> nbits)) ++nbits;
+    int end_bit = std::max(1, std::min(64, 2 * nbits));
+    uint64_t nuniq = 0;
+    if (nkeys) {
+        size_t tmp = 0;
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.as<u64>(), keys2.as<u64>(), (int)nkeys, 0, end_bit, st->stream));
+        G2M_TRY(st->cub_tmp.ensure(tmp));
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(st->cub_tmp.p, tmp, keys.as<u64>(), keys2.as<u64>(), (int)nkeys, 0, end_bit, st->stream));
+        size_t tmp2 = 0;
+        G2M_CUDA(cub::DeviceSelect::Unique(nullptr, tmp2, keys2.as<u64>(), keys.as<u64>(), nk.as<u64>() + 1, (int)nkeys, st->stream));
+        G2M_TRY(st->cub_tmp.ensure(tmp2));
+        G2M_CUDA(cub::DeviceSelect::Unique(st->cub_tmp.p, tmp2, keys2.as<u64>(), keys.as<u64>(), nk.as<u64>() + 1, (int)nkeys, st->stream));
+        G2M_CUDA(cudaMemcpyAsync(&nuniq, nk.as<u64>() + 1, 8, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+    }
+    auto g = std::make_unique<g2m_graph>();
+    g->dev = device;
+    g->nv = n;
+    g->slots = nuniq;
+    G2M_TRY(g->off.ensure((n + 1) * 8));
+    G2M_TRY(g->nbr.ensure(std::max<uint64_t>(nuniq, 1) * 4));
+    if (nuniq) {
+        k_keys_to_csr<<<grid_for(st, nuniq, 256), 256, 0, st->stream>>>(keys.as<u64>(), nuniq, n, g->nbr.as<u32>(), cnt.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), g->off.as<u64>(), n));
+    if (labels) {
+        G2M_TRY(g->labels.ensure(std::max<uint64_t>(n, 1) * 4));
+        if (n) G2M_CUDA(cudaMemcpyAsync(g->labels.p, labels, n * 4, cudaMemcpyHostToDevice, st->stream));
+    }
+    G2M_TRY(finish_graph(g.get(), st));
+    *out = g.release();
+    return G2M_OK;
+}
+
+// ---- reduced edge-task offsets: row v holds |N(v) ∩ [0, v)| tasks (graph.py:275-286)
+
+__global__ void k_red_count(const u64* off, const u32* nbr, u64 nv, u64* cnt) {
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x) {
+        u64 b = off[v], e = off[v + 1];
+        cnt[v] = g2m_lb(nbr + b, (u32)(e - b), (u32)v);
+    }
+}
+
+static int ensure_reduced(const g2m_graph* cg, DevState* st) {
+    g2m_graph* g = const_cast<g2m_graph*>(cg);
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->has_red) return G2M_OK;
+    G2M_TRY(g->red_off.ensure((g->nv + 1) * 8));
+    DevBuf cnt;
+    G2M_TRY(cnt.ensure(std::max<uint64_t>(g->nv, 1) * 8));
+    if (g->nv) {
+        k_red_count<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), g->nv, cnt.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), g->red_off.as<u64>(), g->nv));
+    G2M_CUDA(cudaMemcpyAsync(&g->red_total, g->red_off.as<u64>() + g->nv, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    g->has_red = true;
+    return G2M_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels: NVRTC
+// ---------------------------------------------------------------------------
+
+struct g2m_kernel {
+    g2m_kernel_meta meta;
+    std::string name;
+    std::vector<char> cubin;
+    std::mutex mu;
+    std::map<int, std::pair<CUmodule, CUfunction>> mods;
+    std::map<int, int> occ;   // blocks per SM per device
+};
+
+extern "C" int g2m_kernel_compile(const char* src, const char* name, const char* const* hsrc,
+                                  const char* const* hnames, int32_t nh, const g2m_kernel_meta* meta,
+                                  g2m_kernel** out) {
+    if (!src || !name || !meta || !out) return fail(G2M_EUSAGE, "null argument");
+    nvrtcProgram prog;
+    nvrtcResult r = nvrtcCreateProgram(&prog, src, "g2m_plan.cu", nh, hsrc, hnames);
+    if (r != NVRTC_SUCCESS) return fail(G2M_ECUDA, std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r));
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                          "-default-device", "--device-int128"};
+    r = nvrtcCompileProgram(prog, 5, opts);
+    if (r != NVRTC_SUCCESS) {
+        size_t n = 0;
+        nvrtcGetProgramLogSize(prog, &n);
+        std::string log(n, '\0');
+        nvrtcGetProgramLog(prog, &log[0]);
+        nvrtcDestroyProgram(&prog);
+        return fail(G2M_ECUDA, "NVRTC compile failed:\n" + log);
+    }
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    auto k = std::make_unique<g2m_kernel>();
+    k->cubin.resize(n);
+    nvrtcGetCUBIN(prog, k->cubin.data());
+    nvrtcDestroyProgram(&prog);
+    k->meta = *meta;
+    k->name = name;
+    *out = k.release();
+    return G2M_OK;
+}
+
+extern "C" int g2m_kernel_get_meta(const g2m_kernel* k, g2m_kernel_meta* meta) {
+    if (!k || !meta) return fail(G2M_EUSAGE, "null argument");
+    *meta = k->meta;
+    return G2M_OK;
+}
+
+extern "C" int g2m_kernel_destroy(g2m_kernel* k) {
+    if (!k) return G2M_OK;
+    for (auto& kv : k->mods) {
+        cudaSetDevice(kv.first);
+        if (g_drv.ok) g_drv.ModuleUnload(kv.second.first);
+    }
+    delete k;
+    return G2M_OK;
+}
+
+static int kernel_fn(const g2m_kernel* ck, int dev, DevState* st, CUfunction* fn, int* blocks_per_sm) {
+    g2m_kernel* k = const_cast<g2m_kernel*>(ck);
+    std::lock_guard<std::mutex> lk(k->mu);
+    auto it = k->mods.find(dev);
+    if (it == k->mods.end()) {
+        CUmodule mod;
+        CUfunction f;
+        G2M_CU(ModuleLoadData(&mod, k->cubin.data()));
+        G2M_CU(ModuleGetFunction(&f, mod, k->name.c_str()));
+        const int threads = k->meta.warps_per_block * 32;
+        const size_t smem = (size_t)k->meta.warps_per_block * (size_t)k->meta.warp_words * 4;
+        if (smem > 48 * 1024)
+            G2M_CU(FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem));
+        int occ = 0;
+        G2M_CU(OccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, threads, smem));
+        if (occ < 1) return fail(G2M_ECUDA, "generated kernel cannot be resident (shared memory / registers)");
+        k->occ[dev] = occ;
+        it = k->mods.emplace(dev, std::make_pair(mod, f)).first;
+    }
+    *fn = it->second.second;
+    *blocks_per_sm = k->occ[dev];
+    (void)st;
+    return G2M_OK;
+}
+
+// ---------------------------------------------------------------------------
+// task preparation
+// ---------------------------------------------------------------------------
+
+__global__ void k_pairs_u32(const i64* pairs, u64 m, u32* src, u32* dst) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+        src[i] = (u32)pairs[2 * i];
+        dst[i] = (u32)pairs[2 * i + 1];
+    }
+}
+
+__global__ void k_i64_u32(const i64* in, u64 m, u32* out) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x)
+        out[i] = (u32)in[i];
+}
+
+struct Prepared {
+    G2MArgs a;
+    uint64_t h2d = 0;
+};
+
+static uint64_t rr_local_count(uint64_t total, uint64_t c, uint32_t parts, uint32_t part) {
+    if (c == 0) return total;
+    uint64_t nch = (total + c - 1) / c;
+    if (part >= nch) return 0;
+    uint64_t mine = (nch - part + parts - 1) / parts;   // chunks part, part+parts, ...
+    uint64_t last = part + (mine - 1) * parts;          // index of my last chunk
+    uint64_t last_size = std::min<uint64_t>(c, total - last * c);
+    return (mine - 1) * c + last_size;
+}
+
+static int prepare_tasks(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* ts,
+                         DevState* st, Prepared* P) {
+    G2MArgs& a = P->a;
+    std::memset(&a, 0, sizeof(a));
+    a.off = g->off.as<u64>();
+    a.nbr = g->nbr.as<u32>();
+    a.labels = g->labels.as<u32>();
+    a.nv = g->nv;
+    a.kind = ts->kind;
+    a.source = ts->source;
+    if (ts->kind != k->meta.granularity)
+        return fail(G2M_EUSAGE, ts->kind == G2M_TASKS_EDGE ? "edge tasks supplied to a vertex-parallel forest"
+                                                           : "vertex tasks supplied to an edge-parallel forest");
+    const bool edge = ts->kind == G2M_TASKS_EDGE;
+    if (edge && (ts->source == G2M_SRC_IMPLICIT || ts->source == G2M_SRC_INDEX)) {
+        if (ts->reduced) {
+            G2M_TRY(ensure_reduced(g, st));
+            a.task_off = g->red_off.as<u64>();
+            a.total_implicit = g->red_total;
+        } else {
+            a.task_off = g->off.as<u64>();
+            a.total_implicit = g->slots;
+        }
+    } else if (!edge) {
+        a.total_implicit = g->nv;
+    }
+    switch (ts->source) {
+    case G2M_SRC_IMPLICIT:
+        if (ts->rr_chunk && ts->rr_parts == 0) return fail(G2M_EUSAGE, "rr_parts must be positive");
+        a.rr_chunk = ts->rr_chunk;
+        a.rr_parts = ts->rr_parts;
+        a.rr_part = ts->rr_part;
+        a.ntasks = rr_local_count(a.total_implicit, ts->rr_chunk, ts->rr_parts, ts->rr_part);
+        break;
+    case G2M_SRC_PAIRS: {
+        if (!edge) return fail(G2M_EUSAGE, "edge tasks supplied to a vertex-parallel forest");
+        a.ntasks = ts->count;
+        G2M_TRY(st->tasks_a.ensure(std::max<uint64_t>(ts->count, 1) * 16));
+        G2M_TRY(st->tasks_b.ensure(std::max<uint64_t>(ts->count, 1) * 8));
+        if (ts->count) {
+            G2M_CUDA(cudaMemcpyAsync(st->tasks_a.p, ts->data, ts->count * 16, cudaMemcpyHostToDevice, st->stream));
+            k_pairs_u32<<<grid_for(st, ts->count, 256), 256, 0, st->stream>>>(
+                st->tasks_a.as<i64>(), ts->count, st->tasks_b.as<u32>(), st->tasks_b.as<u32>() + ts->count);
+            G2M_CUDA(cudaGetLastError());
+        }
+        a.t_src = st->tasks_b.as<u32>();
+        a.t_dst = st->tasks_b.as<u32>() + ts->count;
+        P->h2d += ts->count * 16;
+        break;
+    }
+    case G2M_SRC_VERTICES: {
+        if (edge) return fail(G2M_EUSAGE, "vertex tasks supplied to an edge-parallel forest");
+        a.ntasks = ts->count;
+        G2M_TRY(st->tasks_a.ensure(std::max<uint64_t>(ts->count, 1) * 8));
+        G2M_TRY(st->tasks_b.ensure(std::max<uint64_t>(ts->count, 1) * 4));
+        if (ts->count) {
+            G2M_CUDA(cudaMemcpyAsync(st->tasks_a.p, ts->data, ts->count * 8, cudaMemcpyHostToDevice, st->stream));
+            k_i64_u32<<<grid_for(st, ts->count, 256), 256, 0, st->stream>>>(st->tasks_a.as<i64>(), ts->count,
+                                                                               st->tasks_b.as<u32>());
+            G2M_CUDA(cudaGetLastError());
+        }
+        a.t_src = st->tasks_b.as<u32>();
+        P->h2d += ts->count * 8;
+        break;
+    }
+    case G2M_SRC_INDEX: {
+        a.ntasks = ts->count;
+        G2M_TRY(st->tasks_a.ensure(std::max<uint64_t>(ts->count, 1) * 8));
+        if (ts->count)
+            G2M_CUDA(cudaMemcpyAsync(st->tasks_a.p, ts->data, ts->count * 8, cudaMemcpyHostToDevice, st->stream));
+        a.t_index = st->tasks_a.as<u64>();
+        P->h2d += ts->count * 8;
+        break;
+    }
+    default:
+        return fail(G2M_EUSAGE, "unknown task source");
+    }
+    return G2M_OK;
+}
+
+// counters layout (u64 words): [0] next, [1..] counts (2 per pattern), then stats[16]
+static const int kStatsWords = 16;
+
+static int launch(const g2m_kernel* k, const g2m_graph* g, DevState* st, G2MArgs& a,
+                  const g2m_run_config* cfg, uint64_t task_lo, uint64_t task_hi, double* kernel_ms,
+                  uint64_t* warps_out) {
+    CUfunction fn;
+    int occ = 0;
+    G2M_TRY(kernel_fn(k, g->dev, st, &fn, &occ));
+    const int wpb = k->meta.warps_per_block;
+    const size_t smem = (size_t)wpb * (size_t)k->meta.warp_words * 4;
+    int blocks = (cfg && cfg->blocks > 0) ? cfg->blocks : st->sms * occ;
+    // global slot scratch: warps x slots x slot_cap u32
+    const uint64_t nslots = (uint64_t)std::max(k->meta.num_slots, 0);
+    if (nslots && k->meta.smem_slot_cap == 0) {
+        const uint64_t cap = std::max<uint64_t>(g->maxdeg, 1);
+        uint64_t budget = (cfg && cfg->scratch_budget) ? cfg->scratch_budget : (uint64_t)24 << 30;
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        budget = std::min<uint64_t>(budget, free_b > ((size_t)2 << 30) ? free_b - ((size_t)2 << 30) : free_b / 2);
+        uint64_t per_block = (uint64_t)wpb * nslots * cap * 4;
+        uint64_t max_blocks = budget / std::max<uint64_t>(per_block, 1);
+        if (max_blocks < 1) return fail(G2M_EBUDGET, "device memory cannot hold one block's slots");
+        if ((uint64_t)blocks > max_blocks) blocks = (int)max_blocks;
+        G2M_TRY(st->scratch.ensure((uint64_t)blocks * per_block));
+        a.scratch = st->scratch.as<u32>();
+        a.slot_cap = cap;
+    }
+    const uint64_t ntask = task_hi - task_lo;
+    uint64_t grab = (cfg && cfg->chunk) ? cfg->chunk : 0;
+    if (grab == 0) {
+        uint64_t warps = (uint64_t)blocks * wpb;
+        grab = ntask / (warps * 16);
+        if (a.kind == G2M_TASKS_EDGE) grab = std::max<uint64_t>(grab, 1);
+        grab = std::min<uint64_t>(std::max<uint64_t>(grab, 1), 256);
+        if (k->meta.list_mode) grab = 1;
+    }
+    a.grab = grab;
+    u64* ctr = st->counters.as<u64>();
+    a.next = ctr;
+    a.counts = ctr + 1;
+    a.stats = ctr + 1 + 2 * std::max(k->meta.num_patterns, 1);
+    G2M_CUDA(cudaMemcpyAsync(ctr, &task_lo, 8, cudaMemcpyHostToDevice, st->stream));
+    a.ntasks = task_hi;
+    void* params[] = {&a};
+    if (warps_out) *warps_out = (uint64_t)blocks * wpb;
+    G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
+    if (ntask) G2M_CU(LaunchKernel(fn, blocks, 1, 1, wpb * 32, 1, 1, (unsigned)smem, (CUstream)st->stream, params, nullptr));
+    G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
+    G2M_CUDA(cudaEventSynchronize(st->ev1));
+    G2M_CUDA(cudaGetLastError());
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, st->ev0, st->ev1);
+    if (kernel_ms) *kernel_ms += ms;
+    return G2M_OK;
+}
+
+static int reset_counters(const g2m_kernel* k, DevState* st) {
+    const size_t words = 1 + 2 * (size_t)std::max(k->meta.num_patterns, 1) + kStatsWords;
+    G2M_TRY(st->counters.ensure(words * 8));
+    G2M_CUDA(cudaMemsetAsync(st->counters.p, 0, words * 8, st->stream));
+    return G2M_OK;
+}
+
+static int collect(const g2m_kernel* k, DevState* st, uint64_t* counts, g2m_run_stats* stats) {
+    const int np = std::max(k->meta.num_patterns, 1);
+    const size_t words = 1 + 2 * (size_t)np + kStatsWords;
+    std::vector<uint64_t> h(words);
+    G2M_CUDA(cudaMemcpyAsync(h.data(), st->counters.p, words * 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    if (counts)
+        for (int i = 0; i < 2 * k->meta.num_patterns; ++i) counts[i] = h[1 + i];
+    if (stats) {
+        const uint64_t* s = h.data() + 1 + 2 * np;
+        stats->tasks_active = s[0];
+        for (int i = 0; i < 8; ++i) stats->high_water[i] = s[1 + i];
+        stats->alg_bytes_lo = s[9];
+        stats->alg_bytes_hi = s[10];
+        stats->d2h_bytes += words * 8;
+    }
+    return G2M_OK;
+}
+
+extern "C" int g2m_run(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* ts,
+                       const g2m_run_config* cfg, uint64_t* counts, g2m_run_stats* stats) {
+    if (!k || !g || !ts) return fail(G2M_EUSAGE, "null argument");
+    auto t0 = Clock::now();
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    if (k->meta.needs_labels && !g->labels.p) return fail(G2M_EUSAGE, "kernel compiled for a labeled graph");
+    g2m_run_stats local{};
+    g2m_run_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    Prepared P;
+    G2M_TRY(prepare_tasks(k, g, ts, st, &P));
+    G2M_TRY(reset_counters(k, st));
+    S->tasks = P.a.ntasks;
+    G2MArgs a = P.a;
+    G2M_TRY(launch(k, g, st, a, cfg, 0, a.ntasks, &S->kernel_ms, &S->warps));
+    G2M_TRY(collect(k, st, counts, S));
+    S->h2d_bytes += P.h2d;
+    S->total_ms = ms_since(t0);
+    return G2M_OK;
+}
+
+// List mode: a counting pass sizes every task's match stream, then batches
+// of whole tasks are re-run writing tuples at exact offsets, so the host sees
+// matches in reference order (task order, then DFS order).
+extern "C" int g2m_list(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* ts,
+                        const g2m_run_config* cfg, g2m_match_cb cb, void* user, uint64_t* counts,
+                        g2m_run_stats* stats) {
+    if (!k || !g || !ts || !cb) return fail(G2M_EUSAGE, "null argument");
+    if (!k->meta.list_mode) return fail(G2M_EUSAGE, "kernel was not generated for list mode");
+    auto t0 = Clock::now();
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    g2m_run_stats local{};
+    g2m_run_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    Prepared P;
+    G2M_TRY(prepare_tasks(k, g, ts, st, &P));
+    const uint64_t nt = P.a.ntasks;
+    S->tasks = nt;
+    // pass 1: per-task match counts
+    G2M_TRY(reset_counters(k, st));
+    G2M_TRY(st->task_match.ensure(std::max<uint64_t>(nt, 1) * 8));
+    G2M_CUDA(cudaMemsetAsync(st->task_match.p, 0, std::max<uint64_t>(nt, 1) * 8, st->stream));
+    G2MArgs a = P.a;
+    a.task_match = st->task_match.as<u64>();
+    a.task_base = 0;
+    a.list_pass = 0;
+    G2M_TRY(launch(k, g, st, a, cfg, 0, nt, &S->kernel_ms, &S->warps));
+    std::vector<uint64_t> per(nt);
+    if (nt) G2M_CUDA(cudaMemcpyAsync(per.data(), st->task_match.p, nt * 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_TRY(collect(k, st, counts, S));
+    S->d2h_bytes += nt * 8;
+    const int width = k->meta.max_level + 1;
+    const uint64_t cap = std::max<uint64_t>(1, ((uint64_t)64 << 20) / (width * 4));
+    G2M_TRY(st->matches.ensure(cap * width * 4));
+    std::vector<uint32_t> host;
+    std::vector<uint64_t> offs;
+    uint64_t t = 0;
+    int stopped = 0;
+    std::vector<uint64_t> delivered(std::max(k->meta.num_patterns, 1), 0);
+    while (t < nt && !stopped) {
+        // batch [t, e) with total matches <= cap (at least one task)
+        uint64_t e = t, tot = 0;
+        offs.clear();
+        while (e < nt && (e == t || tot + per[e] <= cap)) {
+            offs.push_back(tot);
+            tot += per[e];
+            ++e;
+        }
+        if (tot == 0) { t = e; continue; }
+        if (tot > cap) {
+            G2M_TRY(st->matches.ensure(tot * width * 4));
+        }
+        G2M_CUDA(cudaMemcpyAsync(st->task_match.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, st->stream));
+        G2M_TRY(reset_counters(k, st));
+        G2MArgs b = P.a;
+        b.task_match = st->task_match.as<u64>();
+        b.task_base = t;
+        b.list_pass = 1;
+        b.match_buf = st->matches.as<u32>();
+        b.match_cap = tot;
+        G2M_TRY(launch(k, g, st, b, cfg, t, e, &S->kernel_ms, nullptr));
+        host.resize(tot * width);
+        G2M_CUDA(cudaMemcpyAsync(host.data(), st->matches.p, tot * width * 4, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        S->d2h_bytes += tot * width * 4;
+        // hand over in order; runs of one pattern id per callback
+        uint64_t i = 0;
+        while (i < tot && !stopped) {
+            uint32_t pid = host[i * width];
+            uint64_t j = i + 1;
+            while (j < tot && host[j * width] == pid) ++j;
+            // deliver one at a time so a stop lands on the exact match
+            for (uint64_t q = i; q < j; ++q) {
+                delivered[pid] += 1;
+                int r = cb(user, (int32_t)pid, width - 1, 1, host.data() + q * width + 1);
+                if (r) { stopped = 1; break; }
+            }
+            i = j;
+        }
+        t = e;
+    }
+    if (stopped && counts) {
+        for (int p = 0; p < k->meta.num_patterns; ++p) {
+            counts[2 * p] = delivered[p];
+            counts[2 * p + 1] = 0;
+        }
+    }
+    S->h2d_bytes += P.h2d;
+    S->total_ms = ms_since(t0);
+    return stopped ? G2M_STOPPED : G2M_OK;
+}
+
+// ---------------------------------------------------------------------------
+// batched set operations (setops.py:35-84)
+// ---------------------------------------------------------------------------
+
+__global__ void k_setops(int op, u64 ncase, const u32* av, const u64* ao, const u32* bv, const u64* bo,
+                         const i64* bounds, u64* out_n, u32* out_v) {
+    const u32 lane = g2m_lane();
+    for (u64 c = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; c < ncase;
+         c += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u32* a = av + ao[c];
+        u32 na = (u32)(ao[c + 1] - ao[c]);
+        const u32* b = bv + bo[c];
+        u32 nb = (u32)(bo[c + 1] - bo[c]);
+        const i64 bd = bounds[c];
+        if (bd >= 0) {
+            u32 y = bd > 0xffffffffll ? 0xffffffffu : (u32)bd;
+            na = g2m_wlb(a, na, y);
+            if (op < 2) nb = g2m_wlb(b, nb, y);   // bound_list on both for intersections
+        }
+        const u32 ex[1] = {G2M_NOBOUND};
+        u32 n = 0;
+        if (op == 0 || op == 1) {
+            const u32* lp[2] = {a, b};
+            u32 ln[2] = {na, nb};
+            if (op == 0) n = g2m_materialize<2, 2>(lp, ln, nullptr, 0u, out_v + ao[c]);
+            else n = g2m_count<2, 2, 1>(lp, ln, G2M_NOBOUND, ex, nullptr, 0u);
+        } else {
+            const u32* lp[2] = {a, b};
+            u32 ln[2] = {na, nb};
+            if (op == 2) n = g2m_materialize<1, 2>(lp, ln, nullptr, 0u, out_v + ao[c]);
+            else n = g2m_count<1, 2, 1>(lp, ln, G2M_NOBOUND, ex, nullptr, 0u);
+        }
+        if (lane == 0) out_n[c] = n;
+    }
+}
+
+extern "C" int g2m_setop_batch(int32_t device, int32_t op, uint64_t nc, const uint32_t* av,
+                               const uint64_t* ao, const uint32_t* bv, const uint64_t* bo,
+                               const int64_t* bounds, uint64_t* out_n, uint32_t* out_v) {
+    if (op < 0 || op > 3) return fail(G2M_EUSAGE, "unknown set operation");
+    if (nc == 0) return G2M_OK;
+    DevState* st;
+    G2M_TRY(dev_state(device, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(device));
+    const uint64_t na = ao[nc], nb = bo[nc];
+    DevBuf dav, dao, dbv, dbo, dbd, dn, dv;
+    G2M_TRY(dav.ensure(std::max<uint64_t>(na, 1) * 4));
+    G2M_TRY(dbv.ensure(std::max<uint64_t>(nb, 1) * 4));
+    G2M_TRY(dao.ensure((nc + 1) * 8));
+    G2M_TRY(dbo.ensure((nc + 1) * 8));
+    G2M_TRY(dbd.ensure(nc * 8));
+    G2M_TRY(dn.ensure(nc * 8));
+    G2M_TRY(dv.ensure(std::max<uint64_t>(na, 1) * 4));
+    if (na) G2M_CUDA(cudaMemcpyAsync(dav.p, av, na * 4, cudaMemcpyHostToDevice, st->stream));
+    if (nb) G2M_CUDA(cudaMemcpyAsync(dbv.p, bv, nb * 4, cudaMemcpyHostToDevice, st->stream));
+    G2M_CUDA(cudaMemcpyAsync(dao.p, ao, (nc + 1) * 8, cudaMemcpyHostToDevice, st->stream));
+    G2M_CUDA(cudaMemcpyAsync(dbo.p, bo, (nc + 1) * 8, cudaMemcpyHostToDevice, st->stream));
+    G2M_CUDA(cudaMemcpyAsync(dbd.p, bounds, nc * 8, cudaMemcpyHostToDevice, st->stream));
+    k_setops<<<grid_for(st, nc * 32, 256), 256, 0, st->stream>>>(op, nc, dav.as<u32>(), dao.as<u64>(), dbv.as<u32>(),
+                                                                 dbo.as<u64>(), dbd.as<i64>(), dn.as<u64>(), dv.as<u32>());
+    G2M_CUDA(cudaGetLastError());
+    G2M_CUDA(cudaMemcpyAsync(out_n, dn.p, nc * 8, cudaMemcpyDeviceToHost, st->stream));
+    if (out_v && (op == 0 || op == 2) && na)
+        G2M_CUDA(cudaMemcpyAsync(out_v, dv.p, na * 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return G2M_OK;
+}

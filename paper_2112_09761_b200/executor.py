@@ -1,0 +1,393 @@
+"""Execution operators: ``run_dfs`` and ``run_dfs_lgs`` on the B200.
+
+Same signatures, validation, errors and result types as the reference
+executor (pkg/src/patminer/executor.py:37-106, 339-408, 526-599); the work
+itself is one generated sm_100a kernel per plan forest (``codegen.py``),
+compiled by NVRTC inside libg2m.so and launched through the C ABI
+(``g2m_run`` / ``g2m_list``). There is no host execution path: without the
+native library or a visible GPU these functions raise.
+
+"Workers" keep the reference's meaning for reporting and for the memory
+budget formula (``resolve_worker_count``, executor.py:47-62); on the device
+the unit of parallelism is a resident warp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import codegen
+from .graph import EdgeTaskList, Graph, build_edge_tasks
+from .plan import (EDGE_PARALLEL, EMIT_MATCH, VERTEX_PARALLEL, PlanForest,
+                   SearchPlan, as_forest, emit_source, iter_nodes)
+
+ID_WIDTH = 4  # bytes per vertex id in the worker-budget formula
+
+
+class BudgetError(RuntimeError):
+    """Memory budget cannot fit even a single worker's scratch."""
+
+
+class StopSearch(Exception):
+    """A match sink requested early termination (kept for API parity)."""
+
+
+@dataclass
+class ExecutionConfig:
+    granularity: str = EDGE_PARALLEL
+    workers: int = 1
+    memory_budget: int | None = None     # bytes available for worker scratch
+    lgs: str = "auto"                    # local graph search: auto | on | off
+    lgs_delta_threshold: int = 1024
+    bfs_block_size: int = 1 << 20
+
+
+def resolve_worker_count(cfg: ExecutionConfig, num_buffers: int,
+                         max_degree: int, num_tasks: int) -> int:
+    """min(Y // (X * max_degree * 4), tasks) under a budget Y, else the
+    requested count, clamped to >= 1 (executor.py:47-62)."""
+    if cfg.memory_budget is not None:
+        unit = max(num_buffers, 1) * max(max_degree, 1) * ID_WIDTH
+        cap = cfg.memory_budget // unit
+        if cap < 1:
+            raise BudgetError(f"budget {cfg.memory_budget} B < one worker's scratch ({unit} B)")
+        return max(1, min(int(cap), num_tasks))
+    return max(1, min(cfg.workers, max(num_tasks, 1)))
+
+
+class WorkerContext:
+    """Per-worker counters (executor.py:65-81). On the GPU a worker's scratch
+    is a warp's slots; this host object remains for API compatibility and
+    for merging per-device results."""
+
+    def __init__(self, num_buffers: int, capacity: int, pattern_ids, sink=None):
+        self.scratch = [np.empty(max(capacity, 1), dtype=np.uint32) for _ in range(num_buffers)]
+        self.high_water = [0] * num_buffers
+        self.counts: dict[str, int] = {pid: 0 for pid in pattern_ids}
+        self.sink = sink
+        self.tasks_done = 0
+
+
+def merge_results(contexts: list[WorkerContext]) -> dict[str, int]:
+    total: dict[str, int] = {}
+    for ctx in contexts:
+        for pid, c in ctx.counts.items():
+            total[pid] = total.get(pid, 0) + c
+    return total
+
+
+@dataclass
+class ExecStats:
+    workers: int
+    tasks: int
+    num_buffers: int
+    buffer_high_water: tuple[int, ...]
+    elapsed_s: float
+    kernel_ms: float = 0.0
+    device: int = 0
+    gpu_warps: int = 0
+
+
+@dataclass
+class RunResult:
+    counts: dict[str, int]
+    stats: ExecStats
+    stopped_early: bool = False
+
+
+# ---------------------------------------------------------------------------
+# kernel cache
+# ---------------------------------------------------------------------------
+
+WARPS_PER_BLOCK = 8
+SMEM_SLOT_WORDS = 4096      # per-warp shared-memory budget for slots (u32)
+STAGE_WORDS = 1024          # per-warp staging area for loop-invariant lists
+
+
+class CompiledPlan:
+    """A generated kernel compiled for sm_100a (owned ``g2m_kernel``)."""
+
+    def __init__(self, gen: codegen.GeneratedKernel, handle: int, compile_s: float):
+        self.gen = gen
+        self.handle = handle
+        self.compile_s = compile_s
+
+    def __del__(self):
+        h, self.handle = getattr(self, "handle", None), None
+        if h and N._lib is not None:
+            try:
+                N._lib.g2m_kernel_destroy(h)
+            except Exception:
+                pass
+
+
+_cache: dict[str, CompiledPlan] = {}
+_cache_lock = threading.Lock()
+
+
+def _slot_capacity(forest: PlanForest, labeled: bool, max_degree: int) -> int:
+    slots = codegen.slots_needed(forest, labeled)
+    if slots == 0:
+        return 0
+    cap = 64
+    while cap < max_degree:
+        cap *= 2
+    if slots * cap <= SMEM_SLOT_WORDS:
+        return cap
+    return 0
+
+
+def compile_forest(forest: PlanForest, labeled: bool, list_mode: bool, max_degree: int,
+                   flatten: bool = True) -> CompiledPlan:
+    """Generate + NVRTC-compile (cached by generated source)."""
+    cap = _slot_capacity(forest, labeled, max_degree)
+    gen = codegen.generate(forest, labeled=labeled, list_mode=list_mode,
+                           smem_slot_cap=cap, warps_per_block=WARPS_PER_BLOCK,
+                           stage_words=STAGE_WORDS, flatten=flatten)
+    key = gen.key
+    with _cache_lock:
+        hit = _cache.get(key)
+        if hit is not None:
+            return hit
+        meta = N.KernelMeta()
+        meta.num_patterns = gen.num_patterns
+        meta.num_slots = gen.num_slots
+        meta.granularity = gen.granularity
+        meta.max_level = gen.max_level
+        meta.needs_labels = int(gen.labeled)
+        meta.list_mode = int(gen.list_mode)
+        meta.smem_slot_cap = gen.smem_slot_cap
+        meta.warps_per_block = gen.warps_per_block
+        meta.warp_words = gen.warp_words
+        hsrc, hnames = N.header_sources()
+        arr_src = (C.c_char_p * len(hsrc))(*hsrc)
+        arr_names = (C.c_char_p * len(hnames))(*hnames)
+        h = C.c_void_p()
+        t0 = time.perf_counter()
+        N.check(N.lib().g2m_kernel_compile(gen.source.encode(), gen.name.encode(), arr_src,
+                                           arr_names, len(hsrc), C.byref(meta), C.byref(h)),
+                "kernel compile")
+        cp = CompiledPlan(gen, h.value, time.perf_counter() - t0)
+        _cache[key] = cp
+        return cp
+
+
+# ---------------------------------------------------------------------------
+# task specs
+# ---------------------------------------------------------------------------
+
+class VertexTasks:
+    """The implicit vertex task list ``arange(|V|)`` (executor.py:365-366)."""
+
+    def __init__(self, n: int):
+        self.n = n
+
+    def __len__(self) -> int:
+        return self.n
+
+    def __array__(self, dtype=None, copy=None):
+        return np.arange(self.n, dtype=dtype or np.int64)
+
+
+def task_spec(tasks, *, rr=None, index: np.ndarray | None = None):
+    """Build a ``g2m_task_spec``; returns (spec, keepalive array)."""
+    spec = N.TaskSpec()
+    keep = None
+    if isinstance(tasks, EdgeTaskList):
+        spec.kind = N.TASKS_EDGE
+        spec.reduced = int(bool(tasks.reduced))
+        if index is not None:
+            if not tasks.is_implicit:
+                keep = np.ascontiguousarray(tasks.edges[index], dtype=np.int64)
+                spec.source = N.SRC_PAIRS
+                spec.count = len(keep)
+            else:
+                keep = np.ascontiguousarray(index, dtype=np.int64)
+                spec.source = N.SRC_INDEX
+                spec.count = len(keep)
+        elif tasks.is_implicit:
+            spec.source = N.SRC_IMPLICIT
+        else:
+            keep = np.ascontiguousarray(tasks.edges, dtype=np.int64).reshape(-1, 2)
+            spec.source = N.SRC_PAIRS
+            spec.count = len(keep)
+    else:
+        spec.kind = N.TASKS_VERTEX
+        if isinstance(tasks, VertexTasks) and index is None:
+            spec.source = N.SRC_IMPLICIT
+        else:
+            arr = np.asarray(tasks, dtype=np.int64).reshape(-1)
+            if index is not None:
+                arr = arr[index]
+            keep = np.ascontiguousarray(arr)
+            spec.source = N.SRC_VERTICES
+            spec.count = len(keep)
+    if rr is not None:
+        spec.rr_chunk, spec.rr_parts, spec.rr_part = rr
+    if keep is not None and len(keep):
+        spec.data = keep.ctypes.data_as(C.POINTER(C.c_int64))
+    return spec, keep
+
+
+def _counts_from(words: np.ndarray, pids) -> dict[str, int]:
+    out = {}
+    for i, pid in enumerate(pids):
+        out[pid] = int(words[2 * i]) | (int(words[2 * i + 1]) << 64)
+    return out
+
+
+def _has_emitters(forest: PlanForest) -> bool:
+    return any(a == EMIT_MATCH for r in forest.roots for n in iter_nodes(r)
+               for a, _ in n.actions.values())
+
+
+def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None = None,
+            rr=None, index=None, flatten: bool = True, run_config: N.RunConfig | None = None):
+    """Run one forest on one GPU. Returns (counts, RunStats, stopped, compile)."""
+    dev = N.default_device() if device is None else device
+    N.require_device(dev)
+    dg = g.device_graph(dev)
+    labeled = g.labels is not None
+    list_mode = sink is not None and _has_emitters(forest)
+    cp = compile_forest(forest, labeled, list_mode, dg.max_degree, flatten=flatten)
+    spec, keep = task_spec(tasks, rr=rr, index=index)
+    words = np.zeros(2 * max(cp.gen.num_patterns, 1), dtype=np.uint64)
+    stats = N.RunStats()
+    cfg = run_config if run_config is not None else N.RunConfig()
+    stopped = False
+    if not list_mode:
+        N.check(N.lib().g2m_run(cp.handle, dg.handle, C.byref(spec), C.byref(cfg),
+                                N.ptr(words, C.c_uint64), C.byref(stats)), "run")
+    else:
+        pids = cp.gen.pattern_ids
+        depth = {pid: forest.plans[pid].depth for pid in pids}
+        err: list[BaseException] = []
+
+        def on_match(_user, pid, k, n, tuples):
+            try:
+                name = pids[pid]
+                d = depth[name]
+                for i in range(int(n)):
+                    base = i * k
+                    match = tuple(int(tuples[base + j]) for j in range(d))
+                    if sink(name, match):
+                        return 1
+                return 0
+            except BaseException as exc:  # surface after the native call returns
+                err.append(exc)
+                return 1
+
+        cb = N.MATCH_CB(on_match)
+        rc = N.lib().g2m_list(cp.handle, dg.handle, C.byref(spec), C.byref(cfg), cb, None,
+                              N.ptr(words, C.c_uint64), C.byref(stats))
+        if err:
+            raise err[0]
+        stopped = N.check(rc, "list") == N.G2M_STOPPED
+    del keep
+    return _counts_from(words, cp.gen.pattern_ids), stats, stopped, cp
+
+
+# ---------------------------------------------------------------------------
+# run_dfs / run_dfs_lgs
+# ---------------------------------------------------------------------------
+
+def _default_tasks(g: Graph, forest: PlanForest):
+    if forest.parallel_granularity == EDGE_PARALLEL:
+        plans = list(forest.plans.values())
+        if len(plans) == 1:
+            return build_edge_tasks(g, plans[0])
+        reduced = all(pl.constrains_first_edge() for pl in plans)
+        return EdgeTaskList.implicit(g, reduced=reduced and not g.oriented)
+    return VertexTasks(g.num_vertices)
+
+
+def run_dfs(g: Graph, forest, tasks=None, cfg: ExecutionConfig | None = None,
+            sink=None, device: int | None = None) -> RunResult:
+    """Run a plan or fused forest to completion on one GPU; exact per-pattern
+    counts (executor.py:339-408)."""
+    forest = as_forest(forest)
+    cfg = cfg or ExecutionConfig()
+    if forest.uses_orientation != g.oriented:
+        raise ValueError("plan orientation does not match the graph "
+                         f"(plan={forest.uses_orientation}, graph={g.oriented})")
+    if tasks is None:
+        tasks = _default_tasks(g, forest)
+    edge_mode = isinstance(tasks, EdgeTaskList)
+    if edge_mode and forest.parallel_granularity != EDGE_PARALLEL:
+        raise ValueError("edge tasks supplied to a vertex-parallel forest")
+    if not edge_mode and forest.parallel_granularity != VERTEX_PARALLEL:
+        raise ValueError("vertex tasks supplied to an edge-parallel forest")
+    num_tasks = len(tasks)
+    workers = resolve_worker_count(cfg, forest.num_buffers, g.max_degree, num_tasks)
+    t0 = time.perf_counter()
+    counts, st, stopped, _ = execute(g, forest, tasks, sink=sink, device=device)
+    for pid in forest.pattern_ids:
+        counts.setdefault(pid, 0)
+    high = tuple(int(st.high_water[i]) if i < 8 else 0 for i in range(forest.num_buffers))
+    stats = ExecStats(workers=workers, tasks=num_tasks, num_buffers=forest.num_buffers,
+                      buffer_high_water=high, elapsed_s=time.perf_counter() - t0,
+                      kernel_ms=float(st.kernel_ms),
+                      device=N.default_device() if device is None else device,
+                      gpu_warps=int(st.warps))
+    return RunResult(counts=counts, stats=stats, stopped_early=stopped)
+
+
+def run_dfs_lgs(g: Graph, plan: SearchPlan, tasks=None,
+                cfg: ExecutionConfig | None = None, sink=None,
+                device: int | None = None) -> RunResult:
+    """Hub-rooted plans confined to per-task local graphs (executor.py:526-599).
+    Preconditions and errors are the reference's; counts equal run_dfs."""
+    cfg = cfg or ExecutionConfig()
+    p = plan.pattern
+    k = p.size
+    if p.degree(plan.matching_order.order[0]) != k - 1:
+        raise ValueError("local graph search requires a hub-rooted plan")
+    if plan.uses_orientation != g.oriented:
+        raise ValueError("plan orientation does not match the graph")
+    if any(lv.expr.label is not None for lv in plan.levels):
+        raise ValueError("local graph search does not support label filters")
+    if plan.parallel_granularity == EDGE_PARALLEL:
+        if p.degree(plan.matching_order.order[1]) != k - 1:
+            raise ValueError("edge-parallel local graph search needs hubs at "
+                             "levels 1 and 2; use vertex granularity instead")
+        if tasks is None:
+            tasks = build_edge_tasks(g, plan)
+        anchored = 2
+    else:
+        if tasks is None:
+            tasks = VertexTasks(g.num_vertices)
+        anchored = 1
+    if anchored + 1 > plan.depth:
+        raise ValueError("plan too shallow for local graph search")
+    num_tasks = len(tasks)
+    workers = resolve_worker_count(cfg, plan.num_buffers, g.max_degree, num_tasks)
+    t0 = time.perf_counter()
+    forest = as_forest(plan)
+    counts, st, stopped, _ = execute(g, forest, tasks, sink=sink, device=device)
+    counts = {plan.pattern_id: counts.get(plan.pattern_id, 0)}
+    high = tuple(int(st.high_water[i]) if i < 8 else 0 for i in range(plan.num_buffers))
+    stats = ExecStats(workers=workers, tasks=num_tasks, num_buffers=plan.num_buffers,
+                      buffer_high_water=high, elapsed_s=time.perf_counter() - t0,
+                      kernel_ms=float(st.kernel_ms),
+                      device=N.default_device() if device is None else device,
+                      gpu_warps=int(st.warps))
+    return RunResult(counts=counts, stats=stats, stopped_early=stopped)
+
+
+def describe_kernel(forest, labeled: bool = False, list_mode: bool = False,
+                    max_degree: int = 1024) -> str:
+    """The CUDA source generated for a forest (debug aid, like emit_source)."""
+    f = as_forest(forest)
+    cap = _slot_capacity(f, labeled, max_degree)
+    return codegen.generate(f, labeled=labeled, list_mode=list_mode, smem_slot_cap=cap,
+                            warps_per_block=WARPS_PER_BLOCK, stage_words=STAGE_WORDS).source
+
+
+__all__ = ["BudgetError", "ExecutionConfig", "ExecStats", "RunResult", "StopSearch",
+           "WorkerContext", "merge_results", "resolve_worker_count", "run_dfs",
+           "run_dfs_lgs", "emit_source", "execute", "compile_forest", "VertexTasks"]
