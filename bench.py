@@ -1,0 +1,357 @@
+"""Benchmark: pattern counting on a synthetic RMAT graph on N B200s.
+
+Default workload = BASELINE.json configs[1]: 4-clique counting on RMAT
+scale 22, edge factor 16 (Graph500 a=.57 b=c=.19, seed 1; E = 64,153,257
+undirected edges after dedup), degree-oriented DAG, 1 GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cl4|cl5|tc|c4|diamond]
+                    [--scale 22] [--impl b200|reference]
+
+A step is one complete count pass of the workload's generated kernel over
+the whole (N>1: this rank's chunked round-robin share of the) edge task list
+with the oriented graph resident in HBM. ``value`` = E / step time (edges/s,
+whole job). ``e2e`` runs the same count through the public API
+(``pm.k_clique`` etc.) from pinned host CSR buffers every step: H2D of the
+CSR, device orientation, the kernel, D2H of the counts. ``--impl
+reference`` times the CPU oracle (oracle/oracle.c, the restatement of the
+reference executor) with all host threads on a bounded task sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+WORKLOADS = {
+    "cl4": ("4-clique", "k-clique k=4 count"),
+    "cl5": ("5-clique", "k-clique k=5 count"),
+    "tc": ("triangle", "triangle count"),
+    "c4": ("4-cycle", "subgraph listing 4-cycle count"),
+    "diamond": ("diamond", "subgraph listing diamond count"),
+}
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def make_graph(scale: int, device: int, pinned: bool):
+    """RMAT edges -> CSR built on the GPU -> host copy (pinned)."""
+    import graphs as G
+    from paper_2112_09761_b200 import graph as GR
+    t0 = time.perf_counter()
+    edges = G.rmat_edges(scale, 16, 1)
+    t1 = time.perf_counter()
+    g = GR.from_edges_device(edges, num_vertices=1 << scale, device=device)
+    del edges
+    off, nbr = g.row_offsets, g.neighbors     # downloads once
+    if pinned:
+        import torch
+        po = torch.empty(len(off), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        pn = torch.empty(len(nbr), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        po[:] = off
+        pn[:] = nbr
+        off, nbr = po, pn
+    return g, off, nbr, {"gen_s": t1 - t0, "build_s": time.perf_counter() - t1}
+
+
+def forest_for(workload: str, g):
+    from paper_2112_09761_b200 import pattern as P
+    from paper_2112_09761_b200 import plan as PL
+    if workload in ("cl4", "cl5", "tc"):
+        k = {"cl4": 4, "cl5": 5, "tc": 3}[workload]
+        p = P.generate_clique(k)
+    elif workload == "c4":
+        p = P.Pattern(4, [(0, 1), (1, 2), (2, 3), (3, 0)])
+    else:
+        p = P.Pattern(4, [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3)])
+    mo = P.select_matching_order(P.enumerate_matching_orders(p), P.GraphStats.of(g))
+    so = P.generate_symmetry_order(p, mo)
+    pl = PL.build_plan(p, mo, so, "count", oriented=p.is_clique())
+    pl = PL.apply_counting_rewrite(pl, P.detect_properties(p, mo, so))
+    return PL.as_forest(pl), p
+
+
+def api_call(workload, g):
+    import paper_2112_09761_b200 as pm
+    if workload == "cl4":
+        return pm.k_clique(g, 4).counts
+    if workload == "cl5":
+        return pm.k_clique(g, 5).counts
+    if workload == "tc":
+        return {"triangle": pm.triangle_count(g)}
+    forest, p = forest_for(workload, g)
+    return pm.subgraph_listing(g, p, mode="count").counts
+
+
+def cpu_sample_run(gd, forest, target_s: float, threads: int, seed: int = 7):
+    """Oracle on a seeded uniform sample of the edge task list; returns
+    (seconds, sampled tasks, total tasks, counts)."""
+    from oracle import oracle as O
+    off = np.asarray(gd.row_offsets, dtype=np.int64)
+    nbr = gd.neighbors
+    plans = list(forest.plans.values())
+    reduced = (not gd.oriented) and all(pl.constrains_first_edge() for pl in plans)
+    src_all = None
+    if reduced:
+        src_all = np.repeat(np.arange(gd.num_vertices, dtype=np.int64), np.diff(off))
+        slots = np.flatnonzero(nbr.astype(np.int64) < src_all)
+    else:
+        slots = None
+    total = len(slots) if reduced else int(off[-1])
+    rng = np.random.default_rng(seed)
+
+    def sample(m):
+        pick = rng.choice(total, size=min(m, total), replace=False)
+        pick.sort()
+        s = slots[pick] if reduced else pick
+        src = np.searchsorted(off, s, side="right") - 1
+        return np.column_stack([src, nbr[s].astype(np.int64)])
+
+    m = 2000
+    while True:
+        tasks = sample(m)
+        t0 = time.perf_counter()
+        counts, _ = O.run(gd, forest, tasks=tasks, edge=True, threads=threads)
+        dt = time.perf_counter() - t0
+        if dt >= target_s * 0.5 or m >= total:
+            return dt, len(tasks), total, counts
+        m = int(min(total, m * max(2.0, 0.8 * target_s / max(dt, 1e-3))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cl4", choices=sorted(WORKLOADS))
+    ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    if args.impl == "reference" and rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    pname, desc = WORKLOADS[args.workload]
+    E_expected = None
+    os.environ["G2M_DEVICE"] = str(local)
+    import paper_2112_09761_b200 as pm
+    from paper_2112_09761_b200 import _native as N
+    from paper_2112_09761_b200 import executor as EX
+    from paper_2112_09761_b200 import graph as GR
+
+    g, off_h, nbr_h, build_info = make_graph(args.scale, local, pinned=(args.impl == "b200"))
+    log("graph", build_info, "E", g.num_edges // 2, "maxdeg", g.max_degree)
+    E = g.num_edges // 2
+    forest, pat = forest_for(args.workload, g)
+    gd = GR.orient(g) if pat.is_clique() else g
+    config = {"workload": f"{desc} on RMAT-{args.scale} (ef16, Graph500 a=.57 b=c=.19, seed 1)",
+              "pattern": pname, "graph": f"rmat{args.scale}", "num_vertices": g.num_vertices,
+              "undirected_edges": E, "oriented": gd.oriented, "max_degree_task_graph": gd.max_degree,
+              "parallelism": f"{world} GPU(s), chunked round-robin edge tasks" if world > 1 else "1 GPU",
+              "l2": "inputs larger than L2 (CSR > 126 MB); no flush needed"}
+    metric = "edges/s"
+
+    if args.impl == "reference":
+        threads = os.cpu_count() or 1
+        steps = []
+        for i in range(args.warmup + args.steps):
+            dt, m, total, _ = cpu_sample_run(gd, forest, args.cpu_seconds / 4, threads, seed=100 + i)
+            if i >= args.warmup:
+                steps.append(dt * total / m)
+        t = float(np.mean(steps))
+        v = E / t
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": "edges/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t * 1000.0, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u32 ids / u64 counts", "data": "synthetic RMAT",
+                "config": config,
+                "cpu_baseline": {"value": v, "unit": "edges/s", "cores": threads, "kind": "port",
+                                 "sample": f"uniform seeded edge-task sample per step, extrapolated to all {total} tasks"},
+                "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    # ------------------------------------------------------------------ b200
+    rr = None
+    if world > 1:
+        rr = (256, world, rank)
+    tasks = EX._default_tasks(gd, forest)
+    cp = EX.compile_forest(forest, gd.labels is not None, False, gd.max_degree)
+
+    def step():
+        counts, st, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr)
+        return counts, st
+
+    log("compiled in", round(cp.compile_s, 2), "s; smem/warp words", cp.gen.warp_words,
+        "slots", cp.gen.num_slots, "slot cap", cp.gen.smem_slot_cap)
+    for _ in range(args.warmup):
+        counts, st = step()
+        log("warmup step device_ms", round(st.device_ms, 3), "kernel_ms", round(st.kernel_ms, 3), counts)
+    if dist is not None:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    dev_ms, kern_ms = [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        counts, st = step()
+        dev_ms.append(st.device_ms)
+        kern_ms.append(st.kernel_ms)
+    wall = time.perf_counter() - t0
+    clocks = sampler.stop()
+    my_ms = float(np.mean(dev_ms))
+    total_counts = counts
+    if dist is not None:
+        import torch
+        t = torch.tensor([my_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([[v & 0xFFFFFFFF, v >> 32] for v in counts.values()], dtype=torch.int64,
+                         device=f"cuda:{local}")
+        dist.all_reduce(c)
+        total_counts = {k: int(c[i, 0].item()) + (int(c[i, 1].item()) << 32)
+                        for i, k in enumerate(counts)}
+    else:
+        ms = my_ms
+    value = E / (ms / 1000.0)
+
+    # e2e through the public API from pinned host buffers (N=1), or the
+    # C-ABI upload/orient/run chain per rank (N>1)
+    e2e = None
+    if not args.no_e2e:
+        h2d = off_h.nbytes + nbr_h.nbytes
+        e2e_s = []
+        for i in range(max(1, args.warmup // 2) + args.steps):
+            if dist is not None:
+                dist.barrier()
+            t1 = time.perf_counter()
+            hg = pm.Graph(off_h, nbr_h)
+            if world == 1:
+                c2 = api_call(args.workload, hg)
+            else:
+                hd = GR.orient(hg, device=local) if pat.is_clique() else hg
+                c2, _, _, _ = EX.execute(hd, forest, EX._default_tasks(hd, forest), device=local, rr=rr)
+            dt = time.perf_counter() - t1
+            del hg
+            if i >= max(1, args.warmup // 2):
+                e2e_s.append(dt)
+        e_ms = float(np.mean(e2e_s)) * 1000.0
+        if dist is not None:
+            import torch
+            t = torch.tensor([e_ms], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": E / (e_ms / 1000.0), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(16 * len(counts) + 8 * 32), "ms_per_step": e_ms,
+               "path": "pm.k_clique / triangle_count / subgraph_listing on a fresh host Graph"
+                       if world == 1 else "C-ABI graph_create + orient + run per rank"}
+
+    pk = peaks()
+    hbm = pk.get("hbm_gbs")
+    roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
+            "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6650",
+            "kernel": cp.gen.name, "kernel_share": float(np.mean(kern_ms)) / my_ms if my_ms else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        dt, m, total, _ = cpu_sample_run(gd, forest, args.cpu_seconds, threads)
+        tcpu = dt * total / m
+        cpu = {"value": E / tcpu, "unit": "edges/s", "cores": threads, "kind": "port",
+               "sample": f"{m} of {total} edge tasks (seeded uniform), {dt:.1f}s, extrapolated"}
+
+    line = {"metric": metric, "value": value, "unit": "edges/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32 ids / u64 counts",
+            "data": "synthetic RMAT (seeded; real datasets unavailable offline)",
+            "config": config, "counts": {k: int(v) for k, v in total_counts.items()},
+            "kernel_ms_per_step": float(np.mean(kern_ms)), "wall_s_timed": wall,
+            "gpu_launches": args.steps, "clocks": clocks, "roofline": roof,
+            "cpu_baseline": cpu, "e2e": e2e, "build": build_info,
+            "compile_s": cp.compile_s}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

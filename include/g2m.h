@@ -131,8 +131,11 @@ typedef struct g2m_run_stats {
     uint64_t h2d_bytes;
     uint64_t d2h_bytes;
     uint64_t high_water[8];     /* max materialised size per slot */
-    double kernel_ms;           /* CUDA-event time of the mining kernel */
+    double kernel_ms;           /* CUDA-event time of the mining kernel(s) */
     double total_ms;            /* wall time of the whole call */
+    double device_ms;           /* CUDA-event time of all device work of the call
+                                   after task upload: counter reset, kernel(s),
+                                   result copy-back */
 } g2m_run_stats;
 
 /* Match callback for g2m_list: `n` tuples of `k` vertex ids (level order),

@@ -55,7 +55,7 @@ class RunStats(C.Structure):
                 ("alg_bytes_lo", C.c_uint64), ("alg_bytes_hi", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("high_water", C.c_uint64 * 8), ("kernel_ms", C.c_double),
-                ("total_ms", C.c_double)]
+                ("total_ms", C.c_double), ("device_ms", C.c_double)]
 
     @property
     def alg_bytes(self) -> int:

@@ -91,14 +91,15 @@ def _is_count(action: str) -> bool:
 class _Gen:
     def __init__(self, forest: PlanForest, labeled: bool, list_mode: bool,
                  smem_slot_cap: int, warps_per_block: int, stage_words: int,
-                 flatten: bool):
+                 flatten: bool, instrument: bool = False):
         self.f = forest
+        self.instrument = instrument
         self.labeled = labeled
         self.list_mode = list_mode
         self.smem_cap = smem_slot_cap
         self.wpb = warps_per_block
         self.stage_words = stage_words
-        self.flatten = flatten and not list_mode
+        self.flatten = flatten and not list_mode and not instrument
         if not list_mode:
             forest = _as_counting(forest)
             self.f = forest
@@ -181,6 +182,23 @@ class _Gen:
         else:
             self.o(f"g2m_acc_binom(acc{p}, (u64)({nexpr}), {tail}, a.counts + {2 * p});")
 
+    def balg_stmt(self, expr: SetExpr, count_bound: str | None, full_eval: bool,
+                  cond: str | None = None) -> None:
+        """Instrumentation: add the reference's bytes of _eval / _eval_count."""
+        inter, sub = self.lists(expr)
+        lp = [x[0] for x in inter + sub]
+        ln = [x[1] for x in inter + sub]
+        nb = 1 if expr.base[0] == "nbr" else 0
+        o = self.o
+        o.push(f"if ({cond}) {{" if cond else "{")
+        o(f"const u32* bl[{len(lp)}] = {{{', '.join(lp)}}};")
+        o(f"const u32 bn[{len(ln)}] = {{{', '.join(ln)}}};")
+        if full_eval:
+            o(f"balg += g2m_balg_eval(bl, bn, {len(inter) - 1}, {len(sub)}, {nb});")
+        else:
+            o(f"balg += g2m_balg_evalcount(bl, bn, {len(inter) - 1}, {len(sub)}, {nb}, {count_bound});")
+        o.pop()
+
     # -- leaf terminals (not iterated): _eval_count -----------------------------
 
     def bound_groups(self, node: PlanNode, pids):
@@ -199,6 +217,12 @@ class _Gen:
         lp = [x[0] for x in inter + sub]
         ln = [x[1] for x in inter + sub]
         labp, labv = self.label_args(node.expr)
+        if self.instrument:
+            full = self.labeled and node.expr.label is not None
+            for pid in count_pids:
+                b = node.bounds[pid]
+                self.balg_stmt(node.expr, f"v{b}" if b is not None else "G2M_NOBOUND", full,
+                               cond=f"{mask} & {1 << self.pidx[pid]}u")
         for b, group in self.bound_groups(node, count_pids).items():
             gm = self.mask_of(group)
             o.push(f"if ({mask} & {gm}u) {{")
@@ -383,6 +407,8 @@ class _Gen:
             o(f"s{L}n = g2m_materialize<{len(inter)}, {len(lp)}>(lp, ln, {labp}, {labv}, s{L}p);")
             o.pop()
             child_slot = slot_depth + 1
+        if self.instrument:
+            self.balg_stmt(node.expr, None, True)
         child_buf = buf_depth
         if node.buffered:
             self.hw_levels = max(self.hw_levels, buf_depth + 1)
@@ -424,6 +450,8 @@ class _Gen:
             else:
                 o(f"const u32 {cn} = g2m_wlb(s{L}p, s{L}n, v{b});")
             o(f"if ({mask} & {self.mask_of(group)}u) maxcut = max(maxcut, {cn});")
+        if self.instrument:
+            o("balg += 4ull * maxcut;")
 
         def mask_at(idx_var: str) -> str:
             parts = []
@@ -486,6 +514,8 @@ class _Gen:
     def emit_edge_group(self) -> None:
         """Body for a task group (v1, v2s[0:n2)) -- run_edge_task (executor.py:297-325)."""
         o = self.o
+        if self.instrument:
+            o("balg += 8ull * n2;")
         for root in self.f.roots:
             if root.expr.label is not None and self.labeled:
                 o.push(f"if (__ldg(a.labels + v1) == {int(root.expr.label)}u) {{")
@@ -555,6 +585,8 @@ class _Gen:
     def emit_vertex_task(self) -> None:
         """run_vertex_task (executor.py:284-295)."""
         o = self.o
+        if self.instrument:
+            o("balg += 4;")
         for root in self.f.roots:
             if root.expr.label is not None and self.labeled:
                 o.push(f"if (__ldg(a.labels + v1) == {int(root.expr.label)}u) {{")
@@ -624,6 +656,8 @@ class _Gen:
             w(f"    u32 hw{d} = 0;")
         if self.list_mode:
             w("    u64 mcur = 0;")
+        if self.instrument:
+            w("    u64 balg = 0;")
         w("    u64 row_hint = 0; bool have_hint = false;")
         w("    for (;;) {")
         w("        u64 t0 = 0;")
@@ -684,6 +718,8 @@ class _Gen:
             w(f"    if (lane == 0) g2m_add128(a.counts + {2 * p}, acc{p}, 0);")
         for d in range(min(self.hw_levels, 8)):
             w(f"    if (lane == 0 && hw{d}) atomicMax(a.stats + 1 + {d}, (u64)hw{d});")
+        if self.instrument:
+            w("    if (lane == 0) g2m_add128(a.stats + 9, balg, 0);")
         w("}")
         return GeneratedKernel(
             source="\n".join(src) + "\n", name=KERNEL_NAME, num_patterns=npat,
@@ -746,9 +782,9 @@ def slots_needed(forest: PlanForest, labeled: bool) -> int:
 
 def generate(forest: PlanForest, *, labeled: bool = False, list_mode: bool = False,
              smem_slot_cap: int = 0, warps_per_block: int = 8, stage_words: int = 1024,
-             flatten: bool = True) -> GeneratedKernel:
+             flatten: bool = True, instrument: bool = False) -> GeneratedKernel:
     """Emit the CUDA source of one plan forest. ``smem_slot_cap`` > 0 keeps
     materialised sets in shared memory (capacity in u32 per slot); 0 puts
     them in per-warp global scratch."""
     return _Gen(forest, labeled, list_mode, smem_slot_cap, warps_per_block,
-                stage_words, flatten).generate()
+                stage_words, flatten, instrument).generate()

@@ -138,7 +138,7 @@ struct DevBuf {
 struct DevState {
     std::mutex mu;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
     DevBuf counters;    // next, counts, stats
     DevBuf scratch;     // per-warp slots
     DevBuf tasks_a, tasks_b, task_match, matches, cub_tmp;
@@ -158,6 +158,8 @@ static int dev_state(int dev, DevState** out) {
         G2M_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
         G2M_CUDA(cudaEventCreate(&st->ev0));
         G2M_CUDA(cudaEventCreate(&st->ev1));
+        G2M_CUDA(cudaEventCreate(&st->evs0));
+        G2M_CUDA(cudaEventCreate(&st->evs1));
         G2M_CUDA(cudaDeviceGetAttribute(&st->sms, cudaDevAttrMultiProcessorCount, dev));
         it = g_devs.emplace(dev, std::move(st)).first;
     }
@@ -809,11 +811,19 @@ extern "C" int g2m_run(const g2m_kernel* k, const g2m_graph* g, const g2m_task_s
     std::memset(S, 0, sizeof(*S));
     Prepared P;
     G2M_TRY(prepare_tasks(k, g, ts, st, &P));
+    G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
     G2M_TRY(reset_counters(k, st));
     S->tasks = P.a.ntasks;
     G2MArgs a = P.a;
     G2M_TRY(launch(k, g, st, a, cfg, 0, a.ntasks, &S->kernel_ms, &S->warps));
     G2M_TRY(collect(k, st, counts, S));
+    G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
+    G2M_CUDA(cudaEventSynchronize(st->evs1));
+    {
+        float dm = 0.f;
+        cudaEventElapsedTime(&dm, st->evs0, st->evs1);
+        S->device_ms = dm;
+    }
     S->h2d_bytes += P.h2d;
     S->total_ms = ms_since(t0);
     return G2M_OK;

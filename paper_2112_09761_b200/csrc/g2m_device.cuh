@@ -336,3 +336,99 @@ __device__ __forceinline__ u32 g2m_scan_incl(u32 x) {
     }
     return x;
 }
+
+// ---------------------------------------------------------------------------
+// Instrumentation: SURVEY.md 8(d) algorithmic bytes of the REFERENCE plan
+// (4*(|a|+|b|) per set op as the reference executor passes its operands,
+// 16 per _term call, 4 per DESCEND candidate, 8 / 4 per edge / vertex
+// task). Only compiled into instrumented kernels, which run once outside
+// any timed region to produce the roofline numerator.
+// ---------------------------------------------------------------------------
+
+// |L0 ∩ .. ∩ L(ni-1) - L(ni) - .. - L(nl-1) ∩ [0, bound)| with runtime arity.
+__device__ __noinline__ u32 g2m_count_rt(const u32* const* lp, const u32* ln, int ni, int nl,
+                                         u32 bound) {
+    const u32 lane = g2m_lane();
+    int s = 0;
+    for (int i = 1; i < ni; ++i) if (ln[i] < ln[s]) s = i;
+    const u32* sp = lp[s];
+    u32 sn = ln[s];
+    if (bound != G2M_NOBOUND) sn = g2m_wlb(sp, sn, bound);
+    u32 cnt = 0;
+    for (u32 b = 0; b < sn; b += 32) {
+        u32 i = b + lane;
+        bool ok = i < sn;
+        u32 x = ok ? sp[i] : 0u;
+        for (int j = 0; j < ni && ok; ++j) if (j != s) ok = g2m_has(lp[j], ln[j], x);
+        for (int j = ni; j < nl && ok; ++j) ok = !g2m_has(lp[j], ln[j], x);
+        cnt += __popc(__ballot_sync(G2M_FULL, ok));
+    }
+    return cnt;
+}
+
+// Bytes of _eval(expr) (executor.py:124-140): base (+16 when a neighbour
+// list), intersect terms sorted by length (stable) each +16 when sorted and
+// 4*(|s|+|t|) when applied, then subtract terms +16 and 4*(|s|+|t|).
+// lp/ln: [base, intersect terms..., subtract terms...].
+__device__ __noinline__ u64 g2m_balg_eval(const u32* const* lp_in, const u32* ln_in, int ni_terms,
+                                          int ns, int base_is_nbr) {
+    const u32* lp[9];
+    u32 ln[9];
+    int ord[8];
+    for (int q = 0; q < ni_terms; ++q) ord[q] = q;
+    for (int q = 1; q < ni_terms; ++q) {          // stable insertion sort by length
+        int x = ord[q], r = q - 1;
+        while (r >= 0 && ln_in[1 + ord[r]] > ln_in[1 + x]) { ord[r + 1] = ord[r]; --r; }
+        ord[r + 1] = x;
+    }
+    u64 b = base_is_nbr ? 16 : 0;
+    b += 16ull * (u64)ni_terms;
+    lp[0] = lp_in[0];
+    ln[0] = ln_in[0];
+    u64 cur = ln_in[0];
+    int n = 1;
+    for (int q = 0; q < ni_terms; ++q) {
+        const int t = 1 + ord[q];
+        b += 4ull * (cur + ln_in[t]);
+        lp[n] = lp_in[t];
+        ln[n] = ln_in[t];
+        ++n;
+        cur = g2m_count_rt(lp, ln, n, n, G2M_NOBOUND);
+    }
+    for (int q = 0; q < ns; ++q) {
+        const int t = 1 + ni_terms + q;
+        b += 16 + 4ull * (cur + ln_in[t]);
+        lp[n] = lp_in[t];
+        ln[n] = ln_in[t];
+        ++n;
+        cur = g2m_count_rt(lp, ln, 1 + ni_terms, n, G2M_NOBOUND);
+    }
+    return b;
+}
+
+// Bytes of _eval_count (executor.py:171-194) without a label filter: base
+// (+16 if a neighbour list) cut by the bound, then the ops in expression
+// order (intersections, then subtractions), each +16 and 4*(|s|+|t|).
+__device__ __noinline__ u64 g2m_balg_evalcount(const u32* const* lp_in, const u32* ln_in,
+                                               int ni_terms, int ns, int base_is_nbr, u32 bound) {
+    const u32* lp[9];
+    u32 ln[9];
+    u64 b = base_is_nbr ? 16 : 0;
+    lp[0] = lp_in[0];
+    ln[0] = ln_in[0];
+    u64 cur = (bound != G2M_NOBOUND) ? g2m_wlb(lp_in[0], ln_in[0], bound) : ln_in[0];
+    const int nops = ni_terms + ns;
+    int n = 1;
+    for (int q = 0; q < nops; ++q) {
+        const int t = 1 + q;
+        b += 16 + 4ull * (cur + ln_in[t]);
+        lp[n] = lp_in[t];
+        ln[n] = ln_in[t];
+        ++n;
+        if (q + 1 < nops) {
+            const int ni = (q < ni_terms) ? n : 1 + ni_terms;
+            cur = g2m_count_rt(lp, ln, ni, n, bound);
+        }
+    }
+    return b;
+}

@@ -143,12 +143,12 @@ def _slot_capacity(forest: PlanForest, labeled: bool, max_degree: int) -> int:
 
 
 def compile_forest(forest: PlanForest, labeled: bool, list_mode: bool, max_degree: int,
-                   flatten: bool = True) -> CompiledPlan:
+                   flatten: bool = True, instrument: bool = False) -> CompiledPlan:
     """Generate + NVRTC-compile (cached by generated source)."""
     cap = _slot_capacity(forest, labeled, max_degree)
     gen = codegen.generate(forest, labeled=labeled, list_mode=list_mode,
                            smem_slot_cap=cap, warps_per_block=WARPS_PER_BLOCK,
-                           stage_words=STAGE_WORDS, flatten=flatten)
+                           stage_words=STAGE_WORDS, flatten=flatten, instrument=instrument)
     key = gen.key
     with _cache_lock:
         hit = _cache.get(key)
@@ -164,6 +164,7 @@ def compile_forest(forest: PlanForest, labeled: bool, list_mode: bool, max_degre
         meta.smem_slot_cap = gen.smem_slot_cap
         meta.warps_per_block = gen.warps_per_block
         meta.warp_words = gen.warp_words
+        meta.instrumented = int(instrument)
         hsrc, hnames = N.header_sources()
         arr_src = (C.c_char_p * len(hsrc))(*hsrc)
         arr_names = (C.c_char_p * len(hnames))(*hnames)
@@ -234,6 +235,16 @@ def task_spec(tasks, *, rr=None, index: np.ndarray | None = None):
     return spec, keep
 
 
+def algorithmic_bytes(g: Graph, forest, tasks=None, device: int | None = None) -> int:
+    """SURVEY.md 8(d) algorithmic bytes of the reference plan over `tasks`,
+    from an instrumented variant of the generated kernel (not timed)."""
+    forest = as_forest(forest)
+    if tasks is None:
+        tasks = _default_tasks(g, forest)
+    _, st, _, _ = execute(g, forest, tasks, device=device, instrument=True)
+    return st.alg_bytes
+
+
 def _counts_from(words: np.ndarray, pids) -> dict[str, int]:
     out = {}
     for i, pid in enumerate(pids):
@@ -247,14 +258,16 @@ def _has_emitters(forest: PlanForest) -> bool:
 
 
 def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None = None,
-            rr=None, index=None, flatten: bool = True, run_config: N.RunConfig | None = None):
+            rr=None, index=None, flatten: bool = True, run_config: N.RunConfig | None = None,
+            instrument: bool = False):
     """Run one forest on one GPU. Returns (counts, RunStats, stopped, compile)."""
     dev = N.default_device() if device is None else device
     N.require_device(dev)
     dg = g.device_graph(dev)
     labeled = g.labels is not None
     list_mode = sink is not None and _has_emitters(forest)
-    cp = compile_forest(forest, labeled, list_mode, dg.max_degree, flatten=flatten)
+    cp = compile_forest(forest, labeled, list_mode, dg.max_degree, flatten=flatten,
+                        instrument=instrument)
     spec, keep = task_spec(tasks, rr=rr, index=index)
     words = np.zeros(2 * max(cp.gen.num_patterns, 1), dtype=np.uint64)
     stats = N.RunStats()

@@ -308,3 +308,31 @@ def test_empty_graphs():
     gv = pm.from_edges(np.empty((0, 2), dtype=np.int64), num_vertices=5)
     assert pm.run_dfs(gv, make_plan(P.generate_clique(3))).counts["triangle"] == 0
     assert pm.triangle_count(gv) == 0
+
+
+BALG = json.loads((Path(__file__).parent / "golden" / "balg.json").read_text())
+
+
+@pytest.mark.parametrize("key", sorted(BALG))
+def test_instrumented_kernel_bytes_match_reference(key):
+    """The instrumented generated kernel reproduces the SURVEY 8(d)
+    algorithmic bytes of the instrumented reference exactly."""
+    if key.startswith("er/"):
+        _, n, p, s = key.split("/")
+        g = er(int(n), float(p), int(s))
+    else:
+        g = GR.from_edges(G.rmat_edges(10, 16, 1), num_vertices=1 << 10)
+    for w, want in BALG[key].items():
+        forest, gh = forest_for(w, g)
+        gd = GR.orient(g) if gh.oriented else g
+        assert EX.algorithmic_bytes(gd, forest) == want, (key, w)
+
+
+@pytest.mark.parametrize("workload", ["4-motif", "4-clique", "4-cycle"])
+def test_instrumented_bytes_match_oracle_rmat11(workload):
+    g = GR.from_edges(G.rmat_edges(11 if workload != "4-motif" else 9, 16, 2),
+                      num_vertices=1 << (11 if workload != "4-motif" else 9))
+    forest, gh = forest_for(workload, g)
+    _, want = O.run(gh, forest)
+    gd = GR.orient(g) if gh.oriented else g
+    assert EX.algorithmic_bytes(gd, forest) == want
