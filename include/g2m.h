@@ -172,6 +172,17 @@ int g2m_list(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* tasks
              const g2m_run_config* cfg, g2m_match_cb cb, void* user,
              uint64_t* counts_lo_hi, g2m_run_stats* stats);
 
+/* k-clique count (3 <= k <= 5) on an ORIENTED graph with the bitmap
+ * local-graph kernels (one local DAG per source vertex; setops.py:101-173,
+ * executor.py:415-523). `part` (optional, kind VERTEX, source IMPLICIT with
+ * rr_chunk/rr_parts/rr_part) restricts the sources to a chunked round-robin
+ * share. Sources whose out-degree exceeds the bitmap tiers (> 1024) are
+ * counted by `fallback`, the generated plan kernel of the same k-clique
+ * plan, over their edge tasks. counts_lo_hi receives (lo, hi). */
+int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
+                     const g2m_kernel* fallback, const g2m_run_config* cfg,
+                     uint64_t* counts_lo_hi, g2m_run_stats* stats);
+
 /* Batched sorted-set kernels (setops.py:35-84). Lists are concatenated u32
  * arrays addressed by u64 offsets; op: 0 intersect, 1 intersect_count,
  * 2 difference, 3 difference_count. bound[i] < 0 means "no bound".

@@ -6,6 +6,7 @@
 // offsets, CSR construction, task conversion, batched set operations.
 #include "g2m.h"
 #include "g2m_device.cuh"
+#include "clique_kernels.cuh"
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -921,6 +922,182 @@ extern "C" int g2m_list(const g2m_kernel* k, const g2m_graph* g, const g2m_task_
     S->h2d_bytes += P.h2d;
     S->total_ms = ms_since(t0);
     return stopped ? G2M_STOPPED : G2M_OK;
+}
+
+// ---------------------------------------------------------------------------
+// k-clique via bitmap local graphs
+// ---------------------------------------------------------------------------
+
+__global__ void k_heavy_len(const u64* off, const u32* verts, u64 n, u64* len) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u32 v = verts[i];
+        len[i] = off[v + 1] - off[v];
+    }
+}
+
+__global__ void k_heavy_fill(const u64* off, const u32* verts, u64 n, const u64* pos, u64* idx) {
+    // one warp per heavy vertex: its slot range [off[v], off[v+1]) as task indices
+    const u32 lane = g2m_lane();
+    for (u64 i = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; i < n;
+         i += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u32 v = verts[i];
+        const u64 b = off[v], e = off[v + 1];
+        for (u64 s = b + lane; s < e; s += 32) idx[pos[i] + (s - b)] = s;
+    }
+}
+
+template <int K>
+static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists, u64 stride,
+                             const uint64_t* sizes, u64* ctr, double* kms) {
+    using namespace g2m_clique;
+    const u64* off = g->off.as<u64>();
+    const u32* nbr = g->nbr.as<u32>();
+    u64* count = ctr;        // (lo, hi)
+    u64* next = ctr + 2;     // one work counter per launch
+    int slot = 0;
+    auto timed = [&](auto&& fn) -> int {
+        G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
+        fn();
+        G2M_CUDA(cudaGetLastError());
+        G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
+        G2M_CUDA(cudaEventSynchronize(st->ev1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, st->ev0, st->ev1);
+        *kms += ms;
+        return G2M_OK;
+    };
+    if (sizes[1]) {
+        constexpr int WPB = 8;
+        u64 grab = std::max<u64>(1, std::min<u64>(8, sizes[1] / ((u64)st->sms * 64 * WPB)));
+        G2M_TRY(timed([&] {
+            k_clique_warp<K, WPB><<<st->sms * 8, WPB * 32, 0, st->stream>>>(off, nbr, lists + 1 * stride,
+                                                                            sizes[1], next + slot, grab, count);
+        }));
+        ++slot;
+    }
+    auto cta = [&](auto wtag, int cls) -> int {
+        constexpr int W = decltype(wtag)::value;
+        constexpr int NW = 8;
+        if (!sizes[cls]) return G2M_OK;
+        const size_t smem = (size_t)8 * 64 * W * W + (size_t)4 * 64 * W + (size_t)NW * 4 * (128 + 64 * W);
+        auto kern = k_clique_cta<K, W, NW>;
+        G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
+        const u64 grid = std::min<u64>(sizes[cls], (u64)st->sms * std::max(occ, 1));
+        G2M_TRY(timed([&] {
+            kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
+                                                                 next + slot, count);
+        }));
+        ++slot;
+        return G2M_OK;
+    };
+    G2M_TRY(cta(std::integral_constant<int, 2>{}, 2));
+    G2M_TRY(cta(std::integral_constant<int, 4>{}, 3));
+    G2M_TRY(cta(std::integral_constant<int, 8>{}, 4));
+    G2M_TRY(cta(std::integral_constant<int, 16>{}, 5));
+    return G2M_OK;
+}
+
+extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
+                                const g2m_kernel* fallback, const g2m_run_config* cfg,
+                                uint64_t* counts, g2m_run_stats* stats) {
+    if (!g || !counts) return fail(G2M_EUSAGE, "null argument");
+    if (!g->oriented) return fail(G2M_EUSAGE, "plan orientation does not match the graph");
+    if (k < 3 || k > 5) return fail(G2M_EUSAGE, "bitmap clique kernels cover 3 <= k <= 5");
+    auto t0 = Clock::now();
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    g2m_run_stats local{};
+    g2m_run_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    u64 rr_chunk = 0;
+    u32 parts = 1, pt = 0;
+    if (part && part->rr_chunk) {
+        rr_chunk = part->rr_chunk;
+        parts = part->rr_parts;
+        pt = part->rr_part;
+    }
+    // counters: ctr[8..9] count (lo, hi), ctr[10..] one work counter per launch
+    G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
+    G2M_TRY(st->counters.ensure(32 * 8));
+    u64* ctr = st->counters.as<u64>();
+    // ctr[1], ctr[2]: count; work counters at ctr[8..]
+    G2M_CUDA(cudaMemsetAsync(ctr, 0, 32 * 8, st->stream));
+    const u64 stride = std::max<u64>(g->nv, 1);
+    G2M_TRY(st->tasks_b.ensure(7 * stride * 4));
+    G2M_TRY(st->tasks_a.ensure(8 * 8));
+    u64* dsizes = st->tasks_a.as<u64>();
+    G2M_CUDA(cudaMemsetAsync(dsizes, 0, 8 * 8, st->stream));
+    if (g->nv) {
+        g2m_clique::k_clique_bucket<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(
+            g->off.as<u64>(), g->nv, k - 1, rr_chunk, parts, pt, st->tasks_b.as<u32>(), stride, dsizes);
+        G2M_CUDA(cudaGetLastError());
+    }
+    uint64_t sizes[8];
+    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, 8 * 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    const u32* lists = st->tasks_b.as<u32>();
+    {
+        u64* blk = ctr + 8;
+        int rc;
+        switch (k) {
+        case 3: rc = clique_launch_all<3>(g, st, lists, stride, sizes, blk, &S->kernel_ms); break;
+        case 4: rc = clique_launch_all<4>(g, st, lists, stride, sizes, blk, &S->kernel_ms); break;
+        default: rc = clique_launch_all<5>(g, st, lists, stride, sizes, blk, &S->kernel_ms); break;
+        }
+        if (rc != G2M_OK) return rc;
+    }
+    uint64_t h[2] = {0, 0};
+    G2M_CUDA(cudaMemcpyAsync(h, ctr + 8, 16, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    unsigned __int128 total = ((unsigned __int128)h[1] << 64) | h[0];
+    S->tasks = sizes[1] + sizes[2] + sizes[3] + sizes[4] + sizes[5] + sizes[6];
+    // sources beyond the bitmap tiers: the generated plan kernel over their edge tasks
+    if (sizes[6]) {
+        if (!fallback) return fail(G2M_EUSAGE, "sources with out-degree > 1024 need a fallback kernel");
+        const u64 nh = sizes[6];
+        DevBuf lens, pos, idx;
+        G2M_TRY(lens.ensure(nh * 8));
+        G2M_TRY(pos.ensure((nh + 1) * 8));
+        k_heavy_len<<<grid_for(st, nh, 256), 256, 0, st->stream>>>(g->off.as<u64>(), lists + 6 * stride, nh, lens.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+        G2M_TRY(exclusive_scan_u64(st, lens.as<u64>(), pos.as<u64>(), nh));
+        uint64_t ntask = 0;
+        G2M_CUDA(cudaMemcpyAsync(&ntask, pos.as<u64>() + nh, 8, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        G2M_TRY(idx.ensure(std::max<uint64_t>(ntask, 1) * 8));
+        k_heavy_fill<<<grid_for(st, nh * 32, 256), 256, 0, st->stream>>>(g->off.as<u64>(), lists + 6 * stride, nh,
+                                                                          pos.as<u64>(), idx.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+        G2M_TRY(reset_counters(fallback, st));
+        G2MArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.off = g->off.as<u64>();
+        a.nbr = g->nbr.as<u32>();
+        a.nv = g->nv;
+        a.kind = G2M_TASKS_EDGE;
+        a.source = G2M_SRC_INDEX;
+        a.task_off = g->off.as<u64>();
+        a.total_implicit = g->slots;
+        a.t_index = idx.as<u64>();
+        a.ntasks = ntask;
+        G2M_TRY(launch(fallback, g, st, a, cfg, 0, ntask, &S->kernel_ms, nullptr));
+        uint64_t fc[2] = {0, 0};
+        G2M_TRY(collect(fallback, st, fc, nullptr));
+        total += ((unsigned __int128)fc[1] << 64) | fc[0];
+    }
+    counts[0] = (uint64_t)total;
+    counts[1] = (uint64_t)(total >> 64);
+    G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
+    G2M_CUDA(cudaEventSynchronize(st->evs1));
+    float dm = 0.f;
+    cudaEventElapsedTime(&dm, st->evs0, st->evs1);
+    S->device_ms = dm;
+    S->total_ms = ms_since(t0);
+    return G2M_OK;
 }
 
 // ---------------------------------------------------------------------------

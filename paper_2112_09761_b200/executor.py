@@ -14,6 +14,7 @@ the unit of parallelism is a resident warp.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -252,6 +253,29 @@ def _counts_from(words: np.ndarray, pids) -> dict[str, int]:
     return out
 
 
+# k values routed to the bitmap local-graph clique kernels (g2m_clique_count)
+LGS_CLIQUE_K = {4, 5}
+if os.environ.get("G2M_TC_LGS") == "1":
+    LGS_CLIQUE_K.add(3)
+
+
+def _lgs_clique_k(g: Graph, forest: PlanForest, tasks, sink, index) -> int:
+    """k if this run can use the bitmap clique kernels, else 0: a single
+    count-only clique plan on an oriented, unlabeled graph over its implicit
+    (whole or round-robin) task list."""
+    if len(forest.plans) != 1 or index is not None or g.labels is not None:
+        return 0
+    pl = forest.single()
+    p = pl.pattern
+    if not (p.is_clique() and pl.uses_orientation and g.oriented and p.labels is None):
+        return 0
+    if sink is not None and pl.mode == "list":
+        return 0
+    if not (isinstance(tasks, EdgeTaskList) and tasks.is_implicit):
+        return 0
+    return p.size if p.size in LGS_CLIQUE_K else 0
+
+
 def _has_emitters(forest: PlanForest) -> bool:
     return any(a == EMIT_MATCH for r in forest.roots for n in iter_nodes(r)
                for a, _ in n.actions.values())
@@ -259,12 +283,28 @@ def _has_emitters(forest: PlanForest) -> bool:
 
 def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None = None,
             rr=None, index=None, flatten: bool = True, run_config: N.RunConfig | None = None,
-            instrument: bool = False):
+            instrument: bool = False, lgs: bool = True):
     """Run one forest on one GPU. Returns (counts, RunStats, stopped, compile)."""
     dev = N.default_device() if device is None else device
     N.require_device(dev)
     dg = g.device_graph(dev)
     labeled = g.labels is not None
+    k = 0 if (instrument or not lgs) else _lgs_clique_k(g, forest, tasks, sink, index)
+    if k:
+        # bitmap local-graph kernels; the generated plan kernel handles the
+        # few sources whose out-degree exceeds the bitmap tiers
+        cp = compile_forest(forest, False, False, dg.max_degree, flatten=flatten)
+        spec = N.TaskSpec()
+        spec.kind = N.TASKS_VERTEX
+        if rr is not None:
+            spec.rr_chunk, spec.rr_parts, spec.rr_part = rr
+        words = np.zeros(2, dtype=np.uint64)
+        stats = N.RunStats()
+        cfg = run_config if run_config is not None else N.RunConfig()
+        N.check(N.lib().g2m_clique_count(dg.handle, k, C.byref(spec), cp.handle, C.byref(cfg),
+                                         N.ptr(words, C.c_uint64), C.byref(stats)), "clique")
+        pid = forest.pattern_ids[0]
+        return {pid: int(words[0]) | (int(words[1]) << 64)}, stats, False, cp
     list_mode = sink is not None and _has_emitters(forest)
     cp = compile_forest(forest, labeled, list_mode, dg.max_degree, flatten=flatten,
                         instrument=instrument)

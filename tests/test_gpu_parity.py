@@ -336,3 +336,53 @@ def test_instrumented_bytes_match_oracle_rmat11(workload):
     _, want = O.run(gh, forest)
     gd = GR.orient(g) if gh.oriented else g
     assert EX.algorithmic_bytes(gd, forest) == want
+
+
+def _heavy_source_graph():
+    """A source u with out-degree 1100 (> the 1024 bitmap tier): u links to A
+    (1100 vertices); each a in A gets 1101 private leaves so deg(a) > deg(u);
+    A is internally an ER graph so cliques through u exist."""
+    rng = np.random.default_rng(11)
+    na, leaves = 1100, 1101
+    A = np.arange(1, na + 1)
+    edges = [np.column_stack([np.zeros(na, dtype=np.int64), A])]
+    mask = np.triu(rng.random((na, na)) < 0.02, 1)
+    ii, jj = np.nonzero(mask)
+    edges.append(np.column_stack([A[ii], A[jj]]))
+    base = na + 1
+    src = np.repeat(A, leaves)
+    dst = base + np.arange(na * leaves)
+    edges.append(np.column_stack([src, dst]))
+    e = np.concatenate(edges).astype(np.int64)
+    return GR.from_edges(e, num_vertices=base + na * leaves)
+
+
+@pytest.mark.parametrize("k", [3, 4, 5])
+def test_lgs_clique_kernels_match_generic_and_oracle(k):
+    graphs = [complete(9), complete(70), er(200, 0.08, 21), er(150, 0.3, 5),
+              GR.from_edges(G.rmat_edges(12, 16, 1), num_vertices=1 << 12),
+              GR.from_edges(G.rmat_edges(14, 16, 3), num_vertices=1 << 14),
+              _heavy_source_graph()]
+    for g in graphs:
+        og = GR.orient(g)
+        pl = make_plan(P.generate_clique(k), g, oriented=True)
+        f = PL.as_forest(pl)
+        tasks = EX._default_tasks(og, f)
+        a, _, _, _ = EX.execute(og, f, tasks, lgs=True)
+        b, _, _, _ = EX.execute(og, f, tasks, lgs=False)
+        assert a == b, (g, k)
+        if g.num_edges < 300000:
+            want, _ = O.run(orient_host(g), f)
+            assert a == want
+    assert pm.k_clique(complete(70), 5).counts["5-clique"] == comb(70, 5)
+    assert pm.k_clique(complete(64), 4).counts["4-clique"] == comb(64, 4)
+    assert pm.k_clique(complete(65), 4).counts["4-clique"] == comb(65, 4)
+
+
+def test_rmat12_lgs_known_counts():
+    g = GR.from_edges(G.rmat_edges(12, 16, 1), num_vertices=1 << 12)
+    for k, want in ((3, 480521), (4, 4056943), (5, 27268396)):
+        og = GR.orient(g)
+        f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
+        got, _, _, _ = EX.execute(og, f, EX._default_tasks(og, f), lgs=True)
+        assert got[f.pattern_ids[0]] == want
