@@ -273,7 +273,9 @@ class _Gen:
         labp, labv = self.label_args(child.expr)
         o.push("{")
         o(f"// flattened: {child.expr.render()} over v{L} candidates")
-        # loop-invariant lists; stage small global intersect-side lists
+        # loop-invariant lists: hash the ones that fit into the warp's shared
+        # staging area (membership ~1.5 shared loads); the rest keep a
+        # binary search in global memory
         fixed = inter + sub
         names = []
         for idx, (p, n, is_g) in enumerate(fixed):
@@ -281,16 +283,17 @@ class _Gen:
             o(f"const u32* {fp} = {p}; const u32 {fn} = {n};")
             names.append((fp, fn))
         ninter = len(inter)
-        if ninter and self.stage_words > 0:
+        hashed = []
+        if fixed and self.stage_words > 0:
             self.stage_used = True
             o("u32 stw = 0;")
-            for idx, (p, n, is_g) in enumerate(inter):
-                if not is_g:
-                    continue
+            for idx in range(len(fixed)):
                 fp, fn = names[idx]
-                o.push(f"if ({fn} <= {self.stage_words}u - stw) {{")
-                o(f"{fp} = g2m_stage({fp}, {fn}, stage + stw); stw += {fn};")
-                o.pop()
+                o(f"u32 hl{idx} = 0; u32 ho{idx} = 0;")
+                o(f"if (2u * {fn} <= {self.stage_words}u - stw && {fn} > 8u) "
+                  f"{{ hl{idx} = g2m_hlog({fn}); ho{idx} = stw; stw += 1u << hl{idx}; "
+                  f"g2m_hset_build(stage + ho{idx}, hl{idx}, {fp}, {fn}); }}")
+                hashed.append(idx)
         if ninter:
             o(f"u32 fmin = fn0;")
             for idx in range(1, ninter):
@@ -327,10 +330,10 @@ class _Gen:
         o(f"bool ok = {' && '.join(conds)};")
         for idx in range(len(fixed)):
             fp, fn = names[idx]
-            if idx < ninter:
-                o(f"ok = ok && g2m_has({fp}, {fn}, x);")
-            else:
-                o(f"ok = ok && !g2m_has({fp}, {fn}, x);")
+            search = "g2m_has_g" if fixed[idx][2] else "g2m_has"
+            test = (f"(hl{idx} ? g2m_hset_has(stage + ho{idx}, hl{idx}, x) : {search}({fp}, {fn}, x))"
+                    if idx in hashed else f"{search}({fp}, {fn}, x)")
+            o(f"ok = ok && {'' if idx < ninter else '!'}{test};")
         if labp != "(const u32*)nullptr":
             o(f"ok = ok && __ldg(a.labels + x) == {labv};")
         o.push("if (ok) {")

@@ -23,9 +23,12 @@ namespace g2m_clique {
 
 // Stream the neighbour lists of rows [i0, i0+32) of A, test each element for
 // membership in A (shared, sorted) and set the row bits (row stride W words).
+// A's local ids come from a shared hash map (hk/hv, 2^hl slots); rows have
+// an odd u64 stride W so that lanes reading different rows spread over banks.
 __device__ __forceinline__ void build_rows(const u64* __restrict__ off, const u32* __restrict__ nbr,
                                            const u32* A, u32 d, u32 i0, u64* R, u32 W,
-                                           u32* fl_end, u64* fl_off, u32* fl_row) {
+                                           u32* fl_end, u64* fl_off, u32* fl_row,
+                                           const u32* hk, const u32* hv, u32 hl) {
     const u32 lane = g2m_lane();
     const u32 i = i0 + lane;
     const u32 lo = A[0], hi = A[d - 1];
@@ -55,13 +58,8 @@ __device__ __forceinline__ void build_rows(const u64* __restrict__ off, const u3
         const u32 st = ow ? fl_end[ow - 1] : 0u;
         const u32 x = __ldg(nbr + fl_off[ow] + (e - st));
         if (x >= lo && x <= hi) {
-            u32 pos = 0, n = d;
-            while (n > 1) {
-                const u32 h = n >> 1;
-                pos = (A[pos + h] <= x) ? pos + h : pos;
-                n -= h;
-            }
-            if (A[pos] == x)
+            const u32 pos = g2m_hmap_get(hk, hv, hl, x);
+            if (pos != G2M_EMPTY)
                 atomicOr((unsigned long long*)&R[(u64)fl_row[ow] * W + (pos >> 6)], 1ull << (pos & 63));
         }
     }
@@ -99,6 +97,8 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
     __shared__ u32 sEnd[WPB][32];
     __shared__ __align__(8) u64 sOff[WPB][32];
     __shared__ u32 sRow[WPB][32];
+    __shared__ u32 sHK[WPB][128];
+    __shared__ u32 sHV[WPB][128];
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
     u32* A = sA[w];
@@ -119,8 +119,10 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
             R[lane] = 0;
             R[lane + 32] = 0;
             __syncwarp();
-            build_rows(off, nbr, A, d, 0, R, 1, sEnd[w], sOff[w], sRow[w]);
-            if (d > 32) build_rows(off, nbr, A, d, 32, R, 1, sEnd[w], sOff[w], sRow[w]);
+            const u32 hl = g2m_hlog(d);
+            g2m_hmap_build(sHK[w], sHV[w], hl, A, d, lane, 32);
+            build_rows(off, nbr, A, d, 0, R, 1, sEnd[w], sOff[w], sRow[w], sHK[w], sHV[w], hl);
+            if (d > 32) build_rows(off, nbr, A, d, 32, R, 1, sEnd[w], sOff[w], sRow[w], sHK[w], sHV[w], hl);
             for (u32 i = lane; i < d; i += 32) acc += Chain1<K - 2>::run(R, R[i]);
             __syncwarp();
         }
@@ -137,10 +139,13 @@ __global__ void __launch_bounds__(NW * 32)
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
              u64 nverts, u64* next, u64* count) {
     extern __shared__ __align__(16) u64 smem[];
-    // layout: R [64W x W] u64 | A [64W] u32 | per-warp: end[32] row[32] off[32] list[64W]
+    // layout: R [64W x (W+1)] u64 | A [64W] u32 | hash keys, vals [128W] u32 each |
+    //         per-warp: end[32] row[32] off[32] list[64W]
     u64* R = smem;
-    u32* A = (u32*)(R + 64 * W * W);
-    u32* base = A + 64 * W;
+    u32* A = (u32*)(R + 64 * W * (W + 1));
+    u32* HK = A + 64 * W;
+    u32* HV = HK + 128 * W;
+    u32* base = HV + 128 * W;
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
     u32* fl_end = base + w * (128 + 64 * W);
@@ -158,14 +163,17 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         const u64 b = __ldg(off + u);
         const u32 d = (u32)(__ldg(off + u + 1) - b);
         const u32 Wd = (d + 63) >> 6;
+        const u32 Ws = Wd | 1u;          // odd row stride (bank spread)
         for (u32 x = threadIdx.x; x < d; x += NW * 32) A[x] = __ldg(nbr + b + x);
-        for (u32 x = threadIdx.x; x < d * Wd; x += NW * 32) R[x] = 0;
+        for (u32 x = threadIdx.x; x < d * Ws; x += NW * 32) R[x] = 0;
         __syncthreads();
+        const u32 hl = g2m_hlog(d);
+        g2m_hmap_build(HK, HV, hl, A, d, threadIdx.x, NW * 32);
         for (u32 i0 = w * 32; i0 < d; i0 += NW * 32)
-            build_rows(off, nbr, A, d, i0, R, Wd, fl_end, fl_off, fl_row);
+            build_rows(off, nbr, A, d, i0, R, Ws, fl_end, fl_off, fl_row, HK, HV, hl);
         __syncthreads();
         for (u32 i = w; i < d; i += NW) {
-            const u64* Ri = R + (u64)i * Wd;
+            const u64* Ri = R + (u64)i * Ws;
             if (K == 3) {
                 for (u32 q = lane; q < Wd; q += 32) acc += (u64)__popcll(Ri[q]);
                 continue;
@@ -191,7 +199,7 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
             __syncwarp();
             for (u32 e = lane; e < nl; e += 32) {
                 const u32 j = lst[e];
-                const u64* Rj = R + (u64)j * Wd;
+                const u64* Rj = R + (u64)j * Ws;
                 if (K == 4) {
                     u32 m = nzw;
                     while (m) {
@@ -209,7 +217,7 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                         while (bits) {
                             const u32 l = q * 64 + (__ffsll(bits) - 1);
                             bits &= bits - 1;
-                            const u64* Rl = R + (u64)l * Wd;
+                            const u64* Rl = R + (u64)l * Ws;
 #pragma unroll
                             for (int q2 = 0; q2 < W; ++q2)
                                 if (t2[q2]) acc += (u64)__popcll(t2[q2] & Rl[q2]);

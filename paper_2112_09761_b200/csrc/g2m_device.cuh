@@ -432,3 +432,74 @@ __device__ __noinline__ u64 g2m_balg_evalcount(const u32* const* lp_in, const u3
     }
     return b;
 }
+
+// ---------------------------------------------------------------------------
+// Shared-memory hash sets / maps for loop-invariant lists (open addressing,
+// linear probing, load <= 1/2). Membership then costs ~1.5 shared loads
+// instead of log2(n) dependent probes. Vertex id 0xffffffff marks empty
+// slots (ids are < 2^32 - 1: GCSR graphs have |V| <= 2^32 - 1).
+// ---------------------------------------------------------------------------
+
+#define G2M_EMPTY 0xffffffffu
+
+__device__ __forceinline__ u32 g2m_hslot(u32 x, u32 logcap) {
+    return (x * 0x9E3779B1u) >> (32u - logcap);
+}
+
+// Smallest logcap with 2n <= 2^logcap (>= 1).
+__device__ __forceinline__ u32 g2m_hlog(u32 n) {
+    u32 l = 1;
+    while ((1u << l) < 2u * n) ++l;
+    return l;
+}
+
+// Warp-cooperative build of a set over src[0, n) (src global or shared).
+__device__ __forceinline__ void g2m_hset_build(u32* keys, u32 logcap, const u32* src, u32 n) {
+    const u32 lane = g2m_lane();
+    const u32 cap = 1u << logcap;
+    for (u32 i = lane; i < cap; i += 32) keys[i] = G2M_EMPTY;
+    __syncwarp();
+    for (u32 i = lane; i < n; i += 32) {
+        const u32 x = src[i];
+        u32 h = g2m_hslot(x, logcap);
+        while (atomicCAS(&keys[h], G2M_EMPTY, x) != G2M_EMPTY) h = (h + 1) & (cap - 1);
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ bool g2m_hset_has(const u32* keys, u32 logcap, u32 x) {
+    const u32 mask = (1u << logcap) - 1u;
+    u32 h = g2m_hslot(x, logcap);
+    for (;;) {
+        const u32 k = keys[h];
+        if (k == x) return true;
+        if (k == G2M_EMPTY) return false;
+        h = (h + 1) & mask;
+    }
+}
+
+// Map variant: vals[slot] = position of the key in src (local id).
+__device__ __forceinline__ void g2m_hmap_build(u32* keys, u32* vals, u32 logcap, const u32* src, u32 n,
+                                               u32 tid, u32 nthreads) {
+    const u32 cap = 1u << logcap;
+    for (u32 i = tid; i < cap; i += nthreads) keys[i] = G2M_EMPTY;
+    if (nthreads == 32) __syncwarp(); else __syncthreads();
+    for (u32 i = tid; i < n; i += nthreads) {
+        const u32 x = src[i];
+        u32 h = g2m_hslot(x, logcap);
+        while (atomicCAS(&keys[h], G2M_EMPTY, x) != G2M_EMPTY) h = (h + 1) & (cap - 1);
+        vals[h] = i;
+    }
+    if (nthreads == 32) __syncwarp(); else __syncthreads();
+}
+
+__device__ __forceinline__ u32 g2m_hmap_get(const u32* keys, const u32* vals, u32 logcap, u32 x) {
+    const u32 mask = (1u << logcap) - 1u;
+    u32 h = g2m_hslot(x, logcap);
+    for (;;) {
+        const u32 k = keys[h];
+        if (k == x) return vals[h];
+        if (k == G2M_EMPTY) return G2M_EMPTY;
+        h = (h + 1) & mask;
+    }
+}
