@@ -59,8 +59,8 @@ __device__ __forceinline__ void build_rows(const u64* __restrict__ off, const u3
         const u32 x = __ldg(nbr + fl_off[ow] + (e - st));
         if (x >= lo && x <= hi) {
             const u32 pos = g2m_hmap_get(hk, hv, hl, x);
-            if (pos != G2M_EMPTY)
-                atomicOr((unsigned long long*)&R[(u64)fl_row[ow] * W + (pos >> 6)], 1ull << (pos & 63));
+            if (pos != G2M_EMPTY)   // 32-bit halves: native ATOMS.OR (64-bit would be a CAS loop)
+                atomicOr((u32*)(R + (u64)fl_row[ow] * W) + (pos >> 5), 1u << (pos & 31));
         }
     }
     __syncwarp();
@@ -132,26 +132,30 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
 }
 
 // ---------------------------------------------------------------------------
-// CTA tier: 64 < d <= 64*W, one CTA per source vertex, rows of W words
+// CTA tier: 64 < d <= 64*W, one CTA of NW warps per source vertex, W-word
+// rows with an odd stride. The DFS keeps every lane busy on the bits of one
+// row word at a time (lane l takes bits l and l+32): no per-lane serial
+// chains, so divergence stays low on the dense local graphs of RMAT cores.
 // ---------------------------------------------------------------------------
 template <int K, int W, int NW>
 __global__ void __launch_bounds__(NW * 32)
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
              u64 nverts, u64* next, u64* count) {
     extern __shared__ __align__(16) u64 smem[];
-    // layout: R [64W x (W+1)] u64 | A [64W] u32 | hash keys, vals [128W] u32 each |
-    //         per-warp: end[32] row[32] off[32] list[64W]
+    // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64 | A [64W] u32 |
+    //         hash keys, vals [128W] u32 each | per-warp: end[32] row[32] off[32 u64]
     u64* R = smem;
-    u32* A = (u32*)(R + 64 * W * (W + 1));
+    u64* T = R + 64 * W * (W + 1);
+    u32* A = (u32*)(T + NW * (W + 1));
     u32* HK = A + 64 * W;
     u32* HV = HK + 128 * W;
     u32* base = HV + 128 * W;
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
-    u32* fl_end = base + w * (128 + 64 * W);
+    u32* fl_end = base + w * 128;
     u32* fl_row = fl_end + 32;
     u64* fl_off = (u64*)(fl_end + 64);
-    u32* lst = fl_end + 128;
+    u64* t2s = T + w * (W + 1);
     __shared__ u64 s_u;
     u64 acc = 0;
     for (;;) {
@@ -174,58 +178,64 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         __syncthreads();
         for (u32 i = w; i < d; i += NW) {
             const u64* Ri = R + (u64)i * Ws;
+            const u64 myw = lane < Wd ? Ri[lane] : 0ull;
             if (K == 3) {
-                for (u32 q = lane; q < Wd; q += 32) acc += (u64)__popcll(Ri[q]);
+                acc += (u64)__popcll(myw);
                 continue;
             }
-            // non-zero words of R_i and the set bits of R_i (local list)
-            u32 nzw = 0;     // bitmask of non-zero words (Wd <= 32)
-            u32 nl = 0;
-            for (u32 q0 = 0; q0 < Wd; q0 += 32) {
-                const u32 q = q0 + lane;
-                const u64 word = q < Wd ? Ri[q] : 0ull;
-                const u32 c = (u32)__popcll(word);
-                const u32 incl = g2m_scan_incl(c);
-                const u32 tot = __shfl_sync(G2M_FULL, incl, 31);
-                nzw |= __ballot_sync(G2M_FULL, word != 0ull) << q0;
-                u32 pos = nl + incl - c;
-                u64 bits = word;
-                while (bits) {
-                    lst[pos++] = q * 64 + (__ffsll(bits) - 1);
-                    bits &= bits - 1;
-                }
-                nl += tot;
-            }
-            __syncwarp();
-            for (u32 e = lane; e < nl; e += 32) {
-                const u32 j = lst[e];
-                const u64* Rj = R + (u64)j * Ws;
+            const u32 nzw = __ballot_sync(G2M_FULL, myw != 0ull);
+            u32 wq = nzw;
+            while (wq) {                       // words of R_i holding candidates j
+                const int q = __ffs(wq) - 1;
+                wq &= wq - 1;
+                const u64 word = __shfl_sync(G2M_FULL, myw, q);
                 if (K == 4) {
-                    u32 m = nzw;
-                    while (m) {
-                        const int q = __ffs(m) - 1;
-                        m &= m - 1;
-                        acc += (u64)__popcll(Ri[q] & Rj[q]);
-                    }
-                } else {   // K == 5
-                    u64 t2[W];
 #pragma unroll
-                    for (int q = 0; q < W; ++q) t2[q] = (q < (int)Wd) ? (Ri[q] & Rj[q]) : 0ull;
-#pragma unroll
-                    for (int q = 0; q < W; ++q) {
-                        u64 bits = t2[q];
-                        while (bits) {
-                            const u32 l = q * 64 + (__ffsll(bits) - 1);
-                            bits &= bits - 1;
-                            const u64* Rl = R + (u64)l * Ws;
-#pragma unroll
-                            for (int q2 = 0; q2 < W; ++q2)
-                                if (t2[q2]) acc += (u64)__popcll(t2[q2] & Rl[q2]);
+                    for (int half = 0; half < 2; ++half) {
+                        const u32 bit = lane + 32 * half;
+                        if ((word >> bit) & 1ull) {
+                            const u64* Rj = R + (u64)(q * 64 + bit) * Ws;
+                            u32 m = nzw;
+                            while (m) {
+                                const int q2 = __ffs(m) - 1;
+                                m &= m - 1;
+                                acc += (u64)__popcll(Ri[q2] & Rj[q2]);
+                            }
                         }
                     }
+                } else {                       // K == 5: sequential j, lane-parallel l
+                    u64 bits = word;
+                    while (bits) {
+                        const u32 j = q * 64 + (__ffsll(bits) - 1);
+                        bits &= bits - 1;
+                        const u64* Rj = R + (u64)j * Ws;
+                        const u64 tw = lane < Wd ? (myw & Rj[lane]) : 0ull;
+                        const u32 nz2 = __ballot_sync(G2M_FULL, tw != 0ull);
+                        if (lane < Wd) t2s[lane] = tw;
+                        __syncwarp();
+                        u32 wq2 = nz2;
+                        while (wq2) {
+                            const int q2 = __ffs(wq2) - 1;
+                            wq2 &= wq2 - 1;
+                            const u64 w2 = t2s[q2];
+#pragma unroll
+                            for (int half = 0; half < 2; ++half) {
+                                const u32 bit = lane + 32 * half;
+                                if ((w2 >> bit) & 1ull) {
+                                    const u64* Rl = R + (u64)(q2 * 64 + bit) * Ws;
+                                    u32 m = nz2;
+                                    while (m) {
+                                        const int q3 = __ffs(m) - 1;
+                                        m &= m - 1;
+                                        acc += (u64)__popcll(t2s[q3] & Rl[q3]);
+                                    }
+                                }
+                            }
+                        }
+                        __syncwarp();
+                    }
                 }
             }
-            __syncwarp();
         }
         __syncthreads();
     }

@@ -975,12 +975,12 @@ static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists,
         }));
         ++slot;
     }
-    auto cta = [&](auto wtag, int cls) -> int {
+    auto cta = [&](auto wtag, auto nwtag, int cls) -> int {
         constexpr int W = decltype(wtag)::value;
-        constexpr int NW = 8;
+        constexpr int NW = decltype(nwtag)::value;
         if (!sizes[cls]) return G2M_OK;
-        const size_t smem = (size_t)8 * 64 * W * (W + 1) + (size_t)4 * 64 * W + (size_t)4 * 256 * W +
-                            (size_t)NW * 4 * (128 + 64 * W);
+        const size_t smem = (size_t)8 * (64 * W + NW) * (W + 1) + (size_t)4 * 64 * W + (size_t)4 * 256 * W +
+                            (size_t)NW * 4 * 128;
         auto kern = k_clique_cta<K, W, NW>;
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
@@ -993,10 +993,11 @@ static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists,
         ++slot;
         return G2M_OK;
     };
-    G2M_TRY(cta(std::integral_constant<int, 2>{}, 2));
-    G2M_TRY(cta(std::integral_constant<int, 4>{}, 3));
-    G2M_TRY(cta(std::integral_constant<int, 8>{}, 4));
-    G2M_TRY(cta(std::integral_constant<int, 16>{}, 5));
+    using std::integral_constant;
+    G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 4>{}, 2));
+    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 8>{}, 3));
+    G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, 4));
+    G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, 5));
     return G2M_OK;
 }
 
@@ -1041,6 +1042,10 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, 8 * 8, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     const u32* lists = st->tasks_b.as<u32>();
+    if (getenv("G2M_DEBUG"))
+        fprintf(stderr, "[g2m] clique k=%d buckets: skip<k-1 warp<=64:%llu 128:%llu 256:%llu 512:%llu 1024:%llu >1024:%llu\n",
+                k, (unsigned long long)sizes[1], (unsigned long long)sizes[2], (unsigned long long)sizes[3],
+                (unsigned long long)sizes[4], (unsigned long long)sizes[5], (unsigned long long)sizes[6]);
     {
         u64* blk = ctr + 8;
         int rc;
