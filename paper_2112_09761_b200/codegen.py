@@ -289,10 +289,10 @@ class _Gen:
             o("u32 stw = 0;")
             for idx in range(len(fixed)):
                 fp, fn = names[idx]
-                o(f"u32 hl{idx} = 0; u32 ho{idx} = 0;")
-                o(f"if (2u * {fn} <= {self.stage_words}u - stw && {fn} > 8u) "
-                  f"{{ hl{idx} = g2m_hlog({fn}); ho{idx} = stw; stw += 1u << hl{idx}; "
-                  f"g2m_hset_build(stage + ho{idx}, hl{idx}, {fp}, {fn}); }}")
+                o(f"u32 hl{idx} = {fn} > 8u ? g2m_hlog({fn}) : 0u; u32 ho{idx} = 0;")
+                o(f"if (hl{idx} && (1u << hl{idx}) <= {self.stage_words}u - stw) "
+                  f"{{ ho{idx} = stw; stw += 1u << hl{idx}; "
+                  f"g2m_hset_build(stage + ho{idx}, hl{idx}, {fp}, {fn}); }} else hl{idx} = 0;")
                 hashed.append(idx)
         if ninter:
             o(f"u32 fmin = fn0;")

@@ -203,36 +203,68 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                             }
                         }
                     }
-                } else {                       // K == 5: sequential j, lane-parallel l
-                    u64 bits = word;
-                    while (bits) {
-                        const u32 j = q * 64 + (__ffsll(bits) - 1);
-                        bits &= bits - 1;
-                        const u64* Rj = R + (u64)j * Ws;
-                        const u64 tw = lane < Wd ? (myw & Rj[lane]) : 0ull;
-                        const u32 nz2 = __ballot_sync(G2M_FULL, tw != 0ull);
-                        if (lane < Wd) t2s[lane] = tw;
-                        __syncwarp();
-                        u32 wq2 = nz2;
-                        while (wq2) {
-                            const int q2 = __ffs(wq2) - 1;
-                            wq2 &= wq2 - 1;
-                            const u64 w2 = t2s[q2];
+                } else {
+                    // K == 5: lane per j (t2 = R_i & R_j in registers); j's with
+                    // many common neighbours are handed to the whole warp.
+#pragma unroll 1
+                    for (int half = 0; half < 2; ++half) {
+                        const u32 bit = lane + 32 * half;
+                        const bool isj = (word >> bit) & 1ull;
+                        const u32 j = q * 64 + bit;
+                        u64 t2[W];
+                        u32 c = 0;
 #pragma unroll
-                            for (int half = 0; half < 2; ++half) {
-                                const u32 bit = lane + 32 * half;
-                                if ((w2 >> bit) & 1ull) {
-                                    const u64* Rl = R + (u64)(q2 * 64 + bit) * Ws;
-                                    u32 m = nz2;
-                                    while (m) {
-                                        const int q3 = __ffs(m) - 1;
-                                        m &= m - 1;
-                                        acc += (u64)__popcll(t2s[q3] & Rl[q3]);
-                                    }
+                        for (int r = 0; r < W; ++r) {
+                            t2[r] = (isj && r < (int)Wd) ? (Ri[r] & R[(u64)j * Ws + r]) : 0ull;
+                            c += (u32)__popcll(t2[r]);
+                        }
+                        const bool heavy = c > 48;
+                        if (isj && !heavy) {
+#pragma unroll
+                            for (int r = 0; r < W; ++r) {
+                                u64 bits = t2[r];
+                                while (bits) {
+                                    const u32 l = r * 64 + (__ffsll(bits) - 1);
+                                    bits &= bits - 1;
+                                    const u64* Rl = R + (u64)l * Ws;
+#pragma unroll
+                                    for (int r2 = 0; r2 < W; ++r2)
+                                        if (t2[r2]) acc += (u64)__popcll(t2[r2] & Rl[r2]);
                                 }
                             }
                         }
-                        __syncwarp();
+                        u32 hm = __ballot_sync(G2M_FULL, isj && heavy);
+                        while (hm) {
+                            const int hl = __ffs(hm) - 1;
+                            hm &= hm - 1;
+                            if ((int)lane == hl) {
+#pragma unroll
+                                for (int r = 0; r < W; ++r) if (r < (int)Wd) t2s[r] = t2[r];
+                            }
+                            __syncwarp();
+                            const u64 tw = lane < Wd ? t2s[lane] : 0ull;
+                            const u32 nz2 = __ballot_sync(G2M_FULL, tw != 0ull);
+                            u32 wq2 = nz2;
+                            while (wq2) {
+                                const int q2 = __ffs(wq2) - 1;
+                                wq2 &= wq2 - 1;
+                                const u64 w2 = __shfl_sync(G2M_FULL, tw, q2);
+#pragma unroll
+                                for (int hh = 0; hh < 2; ++hh) {
+                                    const u32 b2 = lane + 32 * hh;
+                                    if ((w2 >> b2) & 1ull) {
+                                        const u64* Rl = R + (u64)(q2 * 64 + b2) * Ws;
+                                        u32 m = nz2;
+                                        while (m) {
+                                            const int q3 = __ffs(m) - 1;
+                                            m &= m - 1;
+                                            acc += (u64)__popcll(t2s[q3] & Rl[q3]);
+                                        }
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                        }
                     }
                 }
             }
