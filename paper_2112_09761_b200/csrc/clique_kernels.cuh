@@ -131,19 +131,39 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
     if (lane == 0 && acc) g2m_add128(count, acc, 0);
 }
 
+// Warp-cooperative compaction of the set bits of words[q0, q1) (shared,
+// read by broadcast) into out[] as bit positions; returns the count.
+__device__ __forceinline__ u32 compact_bits(const u64* words, u32 q0, u32 q1, u32* out) {
+    const u32 lane = g2m_lane();
+    const u32 lt = g2m_lanemask_lt();
+    u32 n = 0;
+    for (u32 q = q0; q < q1; ++q) {
+        const u64 wv = words[q];
+        if (!wv) continue;
+        const u32 lo = (u32)wv, hi = (u32)(wv >> 32);
+        if ((lo >> lane) & 1u) out[n + __popc(lo & lt)] = q * 64 + lane;
+        if ((hi >> lane) & 1u) out[n + __popc(lo) + __popc(hi & lt)] = q * 64 + 32 + lane;
+        n += __popcll(wv);
+    }
+    __syncwarp();
+    return n;
+}
+
 // ---------------------------------------------------------------------------
 // CTA tier: 64 < d <= 64*W, one CTA of NW warps per source vertex, W-word
-// rows with an odd stride. The DFS keeps every lane busy on the bits of one
-// row word at a time (lane l takes bits l and l+32): no per-lane serial
-// chains, so divergence stays low on the dense local graphs of RMAT cores.
+// rows with an odd stride. Each warp takes rows i; the candidates j of R_i
+// are compacted (CH words at a time) into a shared list so every lane gets
+// a candidate. k=5: t2 = R_i & R_j stays in the lane's registers when small;
+// large ones are compacted again and shared by the whole warp.
 // ---------------------------------------------------------------------------
 template <int K, int W, int NW>
 __global__ void __launch_bounds__(NW * 32)
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
              u64 nverts, u64* next, u64* count) {
+    constexpr u32 CH = 4;             // words compacted per round (<= 256 candidates)
     extern __shared__ __align__(16) u64 smem[];
     // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64 | A [64W] u32 |
-    //         hash keys, vals [128W] u32 each | per-warp: end[32] row[32] off[32 u64]
+    //         hash keys, vals [128W] u32 each | per-warp: end[32] row[32] off[32 u64] L1[256] L2[256]
     u64* R = smem;
     u64* T = R + 64 * W * (W + 1);
     u32* A = (u32*)(T + NW * (W + 1));
@@ -152,9 +172,11 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
     u32* base = HV + 128 * W;
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
-    u32* fl_end = base + w * 128;
+    u32* fl_end = base + w * 640;
     u32* fl_row = fl_end + 32;
     u64* fl_off = (u64*)(fl_end + 64);
+    u32* L1 = fl_end + 128;
+    u32* L2 = L1 + 256;
     u64* t2s = T + w * (W + 1);
     __shared__ u64 s_u;
     u64 acc = 0;
@@ -184,41 +206,33 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                 continue;
             }
             const u32 nzw = __ballot_sync(G2M_FULL, myw != 0ull);
-            u32 wq = nzw;
-            while (wq) {                       // words of R_i holding candidates j
-                const int q = __ffs(wq) - 1;
-                wq &= wq - 1;
-                const u64 word = __shfl_sync(G2M_FULL, myw, q);
-                if (K == 4) {
-#pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        const u32 bit = lane + 32 * half;
-                        if ((word >> bit) & 1ull) {
-                            const u64* Rj = R + (u64)(q * 64 + bit) * Ws;
+            if (!nzw) continue;
+            for (u32 c0 = 0; c0 < Wd; c0 += CH) {
+                if (!((nzw >> c0) & ((1u << CH) - 1u))) continue;
+                const u32 n1 = compact_bits(Ri, c0, min(c0 + CH, Wd), L1);
+                for (u32 e0 = 0; e0 < n1; e0 += 32) {
+                    const u32 e = e0 + lane;
+                    const bool isj = e < n1;
+                    const u32 j = isj ? L1[e] : 0u;
+                    const u64* Rj = R + (u64)j * Ws;
+                    if (K == 4) {
+                        if (isj) {
                             u32 m = nzw;
                             while (m) {
-                                const int q2 = __ffs(m) - 1;
+                                const int q = __ffs(m) - 1;
                                 m &= m - 1;
-                                acc += (u64)__popcll(Ri[q2] & Rj[q2]);
+                                acc += (u64)__popcll(Ri[q] & Rj[q]);
                             }
                         }
-                    }
-                } else {
-                    // K == 5: lane per j (t2 = R_i & R_j in registers); j's with
-                    // many common neighbours are handed to the whole warp.
-#pragma unroll 1
-                    for (int half = 0; half < 2; ++half) {
-                        const u32 bit = lane + 32 * half;
-                        const bool isj = (word >> bit) & 1ull;
-                        const u32 j = q * 64 + bit;
+                    } else {   // K == 5
                         u64 t2[W];
                         u32 c = 0;
 #pragma unroll
                         for (int r = 0; r < W; ++r) {
-                            t2[r] = (isj && r < (int)Wd) ? (Ri[r] & R[(u64)j * Ws + r]) : 0ull;
+                            t2[r] = (isj && r < (int)Wd) ? (Ri[r] & Rj[r]) : 0ull;
                             c += (u32)__popcll(t2[r]);
                         }
-                        const bool heavy = c > 48;
+                        const bool heavy = c > 32;
                         if (isj && !heavy) {
 #pragma unroll
                             for (int r = 0; r < W; ++r) {
@@ -235,38 +249,32 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                         }
                         u32 hm = __ballot_sync(G2M_FULL, isj && heavy);
                         while (hm) {
-                            const int hl = __ffs(hm) - 1;
+                            const int hj = __ffs(hm) - 1;
                             hm &= hm - 1;
-                            if ((int)lane == hl) {
+                            if ((int)lane == hj) {
 #pragma unroll
                                 for (int r = 0; r < W; ++r) if (r < (int)Wd) t2s[r] = t2[r];
                             }
                             __syncwarp();
-                            const u64 tw = lane < Wd ? t2s[lane] : 0ull;
-                            const u32 nz2 = __ballot_sync(G2M_FULL, tw != 0ull);
-                            u32 wq2 = nz2;
-                            while (wq2) {
-                                const int q2 = __ffs(wq2) - 1;
-                                wq2 &= wq2 - 1;
-                                const u64 w2 = __shfl_sync(G2M_FULL, tw, q2);
-#pragma unroll
-                                for (int hh = 0; hh < 2; ++hh) {
-                                    const u32 b2 = lane + 32 * hh;
-                                    if ((w2 >> b2) & 1ull) {
-                                        const u64* Rl = R + (u64)(q2 * 64 + b2) * Ws;
-                                        u32 m = nz2;
-                                        while (m) {
-                                            const int q3 = __ffs(m) - 1;
-                                            m &= m - 1;
-                                            acc += (u64)__popcll(t2s[q3] & Rl[q3]);
-                                        }
+                            const u32 nz2 = __ballot_sync(G2M_FULL, lane < Wd && t2s[lane < Wd ? lane : 0] != 0ull);
+                            for (u32 c2 = 0; c2 < Wd; c2 += CH) {
+                                if (!((nz2 >> c2) & ((1u << CH) - 1u))) continue;
+                                const u32 n2 = compact_bits(t2s, c2, min(c2 + CH, Wd), L2);
+                                for (u32 f = lane; f < n2; f += 32) {
+                                    const u64* Rl = R + (u64)L2[f] * Ws;
+                                    u32 m = nz2;
+                                    while (m) {
+                                        const int q3 = __ffs(m) - 1;
+                                        m &= m - 1;
+                                        acc += (u64)__popcll(t2s[q3] & Rl[q3]);
                                     }
                                 }
+                                __syncwarp();
                             }
-                            __syncwarp();
                         }
                     }
                 }
+                __syncwarp();
             }
         }
         __syncthreads();

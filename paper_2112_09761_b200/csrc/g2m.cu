@@ -980,7 +980,7 @@ static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists,
         constexpr int NW = decltype(nwtag)::value;
         if (!sizes[cls]) return G2M_OK;
         const size_t smem = (size_t)8 * (64 * W + NW) * (W + 1) + (size_t)4 * 64 * W + (size_t)4 * 256 * W +
-                            (size_t)NW * 4 * 128;
+                            (size_t)NW * 4 * 640;
         auto kern = k_clique_cta<K, W, NW>;
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
