@@ -191,6 +191,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -268,12 +269,13 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    dev_ms, kern_ms = [], []
+    dev_ms, kern_ms, launches = [], [], 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
         counts, st = step()
         dev_ms.append(st.device_ms)
         kern_ms.append(st.kernel_ms)
+        launches += int(st.launches)
     wall = time.perf_counter() - t0
     clocks = sampler.stop()
     my_ms = float(np.mean(dev_ms))
@@ -324,10 +326,33 @@ def main():
                        if world == 1 else "C-ABI graph_create + orient + run per rank"}
 
     pk = peaks()
-    hbm = pk.get("hbm_gbs")
-    roof = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
-            "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6650",
-            "kernel": cp.gen.name, "kernel_share": float(np.mean(kern_ms)) / my_ms if my_ms else None}
+    hbm = pk.get("hbm_gbs") or 6650.0
+    kms = float(np.mean(kern_ms))
+    # SURVEY 8(d) algorithmic bytes of the reference plan over this rank's
+    # tasks, from the instrumented generated kernel (run once, untimed)
+    balg = None
+    if not args.no_roofline:
+        t_b = time.perf_counter()
+        _, bst, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, instrument=True)
+        balg = int(bst.alg_bytes)
+        log("algorithmic bytes", balg, "in", round(time.perf_counter() - t_b, 2), "s")
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists() and world == 1:
+        traffic = json.loads(tfile.read_text()).get(f"{args.workload}@rmat{args.scale}")
+    achieved = balg / (kms / 1000.0) / 1e9 if balg else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm if achieved else None,
+            "traffic": traffic.get("dram_bytes_per_step") if traffic else None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if pk.get("hbm_gbs") else "fallback 6650 (B200_PROFILING.md)",
+            "algorithmic_bytes_per_step": balg,
+            "algorithmic_bytes_def": "SURVEY 8(d): 4B x (|A|+|B|) per reference set op + 4B per DESCEND candidate + 16B per list opened + 8B per edge task",
+            "kernel": "mining kernels of one step (bitmap LGS tiers + plan kernel)" if pat.is_clique() else cp.gen.name,
+            "kernel_ms_per_step": kms,
+            "kernel_share": kms / my_ms if my_ms else None,
+            "physical_dram_frac": (traffic["dram_bytes_per_step"] / (kms / 1000.0) / 1e9 / hbm)
+            if traffic else None,
+            "traffic_source": traffic.get("source") if traffic else None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -344,7 +369,7 @@ def main():
             "data": "synthetic RMAT (seeded; real datasets unavailable offline)",
             "config": config, "counts": {k: int(v) for k, v in total_counts.items()},
             "kernel_ms_per_step": float(np.mean(kern_ms)), "wall_s_timed": wall,
-            "gpu_launches": args.steps, "clocks": clocks, "roofline": roof,
+            "gpu_launches": launches, "clocks": clocks, "roofline": roof,
             "cpu_baseline": cpu, "e2e": e2e, "build": build_info,
             "compile_s": cp.compile_s}
     if rank == 0:

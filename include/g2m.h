@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define G2M_ABI_VERSION 1
+#define G2M_ABI_VERSION 2
 
 #define G2M_OK 0
 #define G2M_EUSAGE 1
@@ -136,6 +136,7 @@ typedef struct g2m_run_stats {
     double device_ms;           /* CUDA-event time of all device work of the call
                                    after task upload: counter reset, kernel(s),
                                    result copy-back */
+    uint64_t launches;          /* kernels of libg2m launched by the call */
 } g2m_run_stats;
 
 /* Match callback for g2m_list: `n` tuples of `k` vertex ids (level order),

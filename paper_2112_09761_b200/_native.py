@@ -17,6 +17,7 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libg2m.so"
 DEVICE_HEADER = PKG_DIR / "csrc" / "g2m_device.cuh"
 
+ABI_VERSION = 2                     # G2M_ABI_VERSION in include/g2m.h
 G2M_OK, G2M_EUSAGE, G2M_EBUDGET, G2M_ECUDA, G2M_STOPPED = 0, 1, 2, 3, 4
 TASKS_EDGE, TASKS_VERTEX = 0, 1
 SRC_IMPLICIT, SRC_PAIRS, SRC_VERTICES, SRC_INDEX = 0, 1, 2, 3
@@ -55,7 +56,8 @@ class RunStats(C.Structure):
                 ("alg_bytes_lo", C.c_uint64), ("alg_bytes_hi", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("high_water", C.c_uint64 * 8), ("kernel_ms", C.c_double),
-                ("total_ms", C.c_double), ("device_ms", C.c_double)]
+                ("total_ms", C.c_double), ("device_ms", C.c_double),
+                ("launches", C.c_uint64)]
 
     @property
     def alg_bytes(self) -> int:
@@ -120,6 +122,9 @@ def load_library():
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
+            if lib.g2m_abi_version() != ABI_VERSION:
+                raise NativeUnavailable(f"{LIB_PATH} has ABI {lib.g2m_abi_version()}, "
+                                        f"this package needs {ABI_VERSION}; rebuild it")
             _lib = lib
     return _lib
 

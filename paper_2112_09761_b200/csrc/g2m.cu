@@ -144,6 +144,7 @@ struct DevState {
     DevBuf scratch;     // per-warp slots
     DevBuf tasks_a, tasks_b, task_match, matches, cub_tmp;
     int sms = 0;
+    uint64_t launches = 0;   // kernels of ours launched on this device (g2m_run_stats.launches)
 };
 
 static std::mutex g_dev_mu;
@@ -510,6 +511,7 @@ static int ensure_reduced(const g2m_graph* cg, DevState* st) {
     DevBuf cnt;
     G2M_TRY(cnt.ensure(std::max<uint64_t>(g->nv, 1) * 8));
     if (g->nv) {
+        ++st->launches;
         k_red_count<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), g->nv, cnt.as<u64>());
         G2M_CUDA(cudaGetLastError());
     }
@@ -676,6 +678,7 @@ static int prepare_tasks(const g2m_kernel* k, const g2m_graph* g, const g2m_task
         G2M_TRY(st->tasks_b.ensure(std::max<uint64_t>(ts->count, 1) * 8));
         if (ts->count) {
             G2M_CUDA(cudaMemcpyAsync(st->tasks_a.p, ts->data, ts->count * 16, cudaMemcpyHostToDevice, st->stream));
+            ++st->launches;
             k_pairs_u32<<<grid_for(st, ts->count, 256), 256, 0, st->stream>>>(
                 st->tasks_a.as<i64>(), ts->count, st->tasks_b.as<u32>(), st->tasks_b.as<u32>() + ts->count);
             G2M_CUDA(cudaGetLastError());
@@ -692,6 +695,7 @@ static int prepare_tasks(const g2m_kernel* k, const g2m_graph* g, const g2m_task
         G2M_TRY(st->tasks_b.ensure(std::max<uint64_t>(ts->count, 1) * 4));
         if (ts->count) {
             G2M_CUDA(cudaMemcpyAsync(st->tasks_a.p, ts->data, ts->count * 8, cudaMemcpyHostToDevice, st->stream));
+            ++st->launches;
             k_i64_u32<<<grid_for(st, ts->count, 256), 256, 0, st->stream>>>(st->tasks_a.as<i64>(), ts->count,
                                                                                st->tasks_b.as<u32>());
             G2M_CUDA(cudaGetLastError());
@@ -762,6 +766,7 @@ static int launch(const g2m_kernel* k, const g2m_graph* g, DevState* st, G2MArgs
     void* params[] = {&a};
     if (warps_out) *warps_out = (uint64_t)blocks * wpb;
     G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
+    if (ntask) ++st->launches;
     if (ntask) G2M_CU(LaunchKernel(fn, blocks, 1, 1, wpb * 32, 1, 1, (unsigned)smem, (CUstream)st->stream, params, nullptr));
     G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
     G2M_CUDA(cudaEventSynchronize(st->ev1));
@@ -810,6 +815,7 @@ extern "C" int g2m_run(const g2m_kernel* k, const g2m_graph* g, const g2m_task_s
     g2m_run_stats local{};
     g2m_run_stats* S = stats ? stats : &local;
     std::memset(S, 0, sizeof(*S));
+    const uint64_t l0 = st->launches;
     Prepared P;
     G2M_TRY(prepare_tasks(k, g, ts, st, &P));
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
@@ -826,6 +832,7 @@ extern "C" int g2m_run(const g2m_kernel* k, const g2m_graph* g, const g2m_task_s
         S->device_ms = dm;
     }
     S->h2d_bytes += P.h2d;
+    S->launches = st->launches - l0;
     S->total_ms = ms_since(t0);
     return G2M_OK;
 }
@@ -846,6 +853,7 @@ extern "C" int g2m_list(const g2m_kernel* k, const g2m_graph* g, const g2m_task_
     g2m_run_stats local{};
     g2m_run_stats* S = stats ? stats : &local;
     std::memset(S, 0, sizeof(*S));
+    const uint64_t l0 = st->launches;
     Prepared P;
     G2M_TRY(prepare_tasks(k, g, ts, st, &P));
     const uint64_t nt = P.a.ntasks;
@@ -920,6 +928,7 @@ extern "C" int g2m_list(const g2m_kernel* k, const g2m_graph* g, const g2m_task_
         }
     }
     S->h2d_bytes += P.h2d;
+    S->launches = st->launches - l0;
     S->total_ms = ms_since(t0);
     return stopped ? G2M_STOPPED : G2M_OK;
 }
@@ -970,6 +979,7 @@ static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists,
         constexpr int WPB = 8;
         u64 grab = std::max<u64>(1, std::min<u64>(8, sizes[1] / ((u64)st->sms * 64 * WPB)));
         G2M_TRY(timed([&] {
+            ++st->launches;
             k_clique_warp<K, WPB><<<st->sms * 8, WPB * 32, 0, st->stream>>>(off, nbr, lists + 1 * stride,
                                                                             sizes[1], next + slot, grab, count);
         }));
@@ -987,6 +997,7 @@ static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists,
         G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
         const u64 grid = std::min<u64>(sizes[cls], (u64)st->sms * std::max(occ, 1));
         G2M_TRY(timed([&] {
+            ++st->launches;
             kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
                                                                  next + slot, count);
         }));
@@ -1015,6 +1026,7 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     g2m_run_stats local{};
     g2m_run_stats* S = stats ? stats : &local;
     std::memset(S, 0, sizeof(*S));
+    const uint64_t l0 = st->launches;
     u64 rr_chunk = 0;
     u32 parts = 1, pt = 0;
     if (part && part->rr_chunk) {
@@ -1034,6 +1046,7 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     u64* dsizes = st->tasks_a.as<u64>();
     G2M_CUDA(cudaMemsetAsync(dsizes, 0, 8 * 8, st->stream));
     if (g->nv) {
+        ++st->launches;
         g2m_clique::k_clique_bucket<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(
             g->off.as<u64>(), g->nv, k - 1, rr_chunk, parts, pt, st->tasks_b.as<u32>(), stride, dsizes);
         G2M_CUDA(cudaGetLastError());
@@ -1068,6 +1081,7 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
         DevBuf lens, pos, idx;
         G2M_TRY(lens.ensure(nh * 8));
         G2M_TRY(pos.ensure((nh + 1) * 8));
+        ++st->launches;
         k_heavy_len<<<grid_for(st, nh, 256), 256, 0, st->stream>>>(g->off.as<u64>(), lists + 6 * stride, nh, lens.as<u64>());
         G2M_CUDA(cudaGetLastError());
         G2M_TRY(exclusive_scan_u64(st, lens.as<u64>(), pos.as<u64>(), nh));
@@ -1075,6 +1089,7 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
         G2M_CUDA(cudaMemcpyAsync(&ntask, pos.as<u64>() + nh, 8, cudaMemcpyDeviceToHost, st->stream));
         G2M_CUDA(cudaStreamSynchronize(st->stream));
         G2M_TRY(idx.ensure(std::max<uint64_t>(ntask, 1) * 8));
+        ++st->launches;
         k_heavy_fill<<<grid_for(st, nh * 32, 256), 256, 0, st->stream>>>(g->off.as<u64>(), lists + 6 * stride, nh,
                                                                           pos.as<u64>(), idx.as<u64>());
         G2M_CUDA(cudaGetLastError());
@@ -1102,6 +1117,7 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     float dm = 0.f;
     cudaEventElapsedTime(&dm, st->evs0, st->evs1);
     S->device_ms = dm;
+    S->launches = st->launches - l0;
     S->total_ms = ms_since(t0);
     return G2M_OK;
 }

@@ -27,13 +27,13 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(N.SIGNATURES)
-    assert lib.g2m_abi_version() == 1
+    assert lib.g2m_abi_version() == 2
 
 
 def test_struct_layouts():
     assert C.sizeof(N.TaskSpec) == 48
     assert C.sizeof(N.KernelMeta) == 64
-    assert C.sizeof(N.RunStats) == 8 * 15 + 24
+    assert C.sizeof(N.RunStats) == 8 * 16 + 24
 
 
 def _forests():
