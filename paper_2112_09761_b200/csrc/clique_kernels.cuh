@@ -1,19 +1,27 @@
 // clique_kernels.cuh -- bitmap local-graph search (LGS) for k-clique counting
-// on the degree-oriented DAG (G²Miner LGS; reference
-// _LocalRunner executor.py:415-523, setops.build_local_graph
+// (k = 3..5) on the degree-oriented DAG (G²Miner LGS, PAPER.md:1040-1075;
+// reference _LocalRunner executor.py:415-523, setops.build_local_graph
 // setops.py:124-142, mask/popcount helpers setops.py:145-173).
 //
-// Every k-clique of an oriented graph has a unique source u (its minimum in
-// the (degree, id) order). With A = N+(u) renamed to local ids 0..d-1
-// (ascending ids, as the reference's LocalGraph), row R[i] is the bitmap of
+// Every k-clique of a DAG has a unique source u (the vertex all others are
+// out-neighbours of). With A = N+(u) renamed to local ids 0..d-1 (ascending
+// ids, as the reference's LocalGraph), row R[i] is the bitmap of
 // A ∩ N+(A[i]); the k-cliques with source u are exactly the (k-1)-cliques of
 // the local DAG R, counted with AND + popcount:
 //   k=3: Σ_i |R_i|     k=4: Σ_i Σ_{j∈R_i} |R_i & R_j|
 //   k=5: Σ_i Σ_{j∈R_i} Σ_{l∈R_i&R_j} |R_i & R_j & R_l|
 // so counts equal the reference's sorted-list plan (the same cliques).
 //
-// Tiers: d <= 64 -> one warp per source, single-word rows in shared memory;
-// 64 < d <= 64*W -> one CTA per source, W-word rows in shared memory.
+// The kernels run on the rank-space copy of the DAG (g2m.cu ensure_rank):
+// ids are positions in the (degree, id) order, so every out-neighbour has a
+// larger id and A spans a narrow window [A0, A_last] for the sources of the
+// CTA tiers. Membership + local id of a probed id x is then a direct-address
+// lookup in a shared-memory bitmap of that window (one LDS, one POPC, no
+// probing loop, no divergence); a linear-probing hash map is the fallback
+// for windows wider than the bitmap.
+//
+// Tiers: d <= 64 -> one warp per source, hash map, single-word rows;
+// 64 < d <= 64*W -> one CTA of NW warps per source, W-word rows.
 // Sources with d > 1024 are left to the generic plan kernel.
 #pragma once
 
@@ -21,49 +29,84 @@
 
 namespace g2m_clique {
 
-// Stream the neighbour lists of rows [i0, i0+32) of A, test each element for
-// membership in A (shared, sorted) and set the row bits (row stride W words).
-// A's local ids come from a shared hash map (hk/hv, 2^hl slots); rows have
-// an odd u64 stride W so that lanes reading different rows spread over banks.
-__device__ __forceinline__ void build_rows(const u64* __restrict__ off, const u32* __restrict__ nbr,
-                                           const u32* A, u32 d, u32 i0, u64* R, u32 W,
-                                           u32* fl_end, u64* fl_off, u32* fl_row,
-                                           const u32* hk, const u32* hv, u32 hl) {
+typedef unsigned short u16;
+
+// ---- probe structures: local id of x in A, or G2M_EMPTY -------------------
+
+struct BitmapProbe {          // direct-address window [base, base + span)
+    const u32* bm;            // span bits
+    const u16* pre;           // local id of the first member of each word
+    u32 base, span;
+    __device__ __forceinline__ u32 get(u32 x) const {
+        const u32 o = x - base;                    // wraps for x < base
+        if (o >= span) return G2M_EMPTY;
+        const u32 w = bm[o >> 5];
+        const u32 b = 1u << (o & 31u);
+        if (!(w & b)) return G2M_EMPTY;
+        return (u32)pre[o >> 5] + (u32)__popc(w & (b - 1u));
+    }
+    __device__ __forceinline__ bool has(u32 x) const {
+        const u32 o = x - base;
+        return o < span && ((bm[o >> 5] >> (o & 31u)) & 1u);
+    }
+};
+
+struct HashProbe {            // linear probing, load <= 1/2
+    const u32* hk;
+    const u32* hv;
+    u32 hl, lo, hi;
+    __device__ __forceinline__ u32 get(u32 x) const {
+        if (x < lo || x > hi) return G2M_EMPTY;
+        return g2m_hmap_get(hk, hv, hl, x);
+    }
+    __device__ __forceinline__ bool has(u32 x) const { return get(x) != G2M_EMPTY; }
+};
+
+// Warp tier: probe the out-lists of rows [i0, i0+32) of A (scratch: 128
+// words: end[32] row[32] base[32 u64]). K == 3 returns the number of
+// members found (triangles u, A[i], x); otherwise sets the row bits of R
+// (row stride Ws words) and returns 0. All 32 lanes share the concatenated
+// lists (load-balanced whatever the list lengths).
+template <int K, typename Probe>
+__device__ __forceinline__ u32 probe_rows(const u64* __restrict__ off, const u32* __restrict__ nbr,
+                                          const u32* A, u32 d, u32 i0, u64* R, u32 Ws,
+                                          u32* scratch, const Probe& P) {
     const u32 lane = g2m_lane();
+    u32* fl_end = scratch;
+    u32* fl_row = scratch + 32;
+    u64* fl_base = (u64*)(scratch + 64);
     const u32 i = i0 + lane;
-    const u32 lo = A[0], hi = A[d - 1];
+    const u32 hi = A[d - 1];
     u64 ro = 0;
     u32 rn = 0;
     if (i < d) {
         const u32 v = A[i];
         ro = __ldg(off + v);
         rn = (u32)(__ldg(off + v + 1) - ro);
-        if (rn > 48) {   // cut the parts of long lists that cannot hit [A0, A(d-1)]
-            const u32* p = nbr + ro;
-            const u32 s = g2m_lb(p, rn, lo);
-            const u32 e = g2m_lb(p, rn, hi + 1u);
-            ro += s;
-            rn = e - s;
-        }
+        // out-neighbours of v are > v >= A0; drop the tail beyond A_last
+        if (rn > 32 && __ldg(nbr + ro + rn - 1) > hi) rn = g2m_lb(nbr + ro, rn, hi + 1u);
     }
     const u32 incl = g2m_scan_incl(rn);
     const u32 tot = __shfl_sync(G2M_FULL, incl, 31);
     fl_end[lane] = incl;
-    fl_off[lane] = ro;
     fl_row[lane] = i;
+    fl_base[lane] = ro - (u64)(incl - rn);     // nbr index of flattened position e = base + e
     __syncwarp();
+    u32 hits = 0;
     u32 ow = 0;
     for (u32 e = lane; e < tot; e += 32) {
         while (fl_end[ow] <= e) ++ow;
-        const u32 st = ow ? fl_end[ow - 1] : 0u;
-        const u32 x = __ldg(nbr + fl_off[ow] + (e - st));
-        if (x >= lo && x <= hi) {
-            const u32 pos = g2m_hmap_get(hk, hv, hl, x);
+        const u32 x = __ldg(nbr + (fl_base[ow] + e));
+        if constexpr (K == 3) {
+            hits += P.has(x) ? 1u : 0u;
+        } else {
+            const u32 pos = P.get(x);
             if (pos != G2M_EMPTY)   // 32-bit halves: native ATOMS.OR (64-bit would be a CAS loop)
-                atomicOr((u32*)(R + (u64)fl_row[ow] * W) + (pos >> 5), 1u << (pos & 31));
+                atomicOr((u32*)(R + (u64)fl_row[ow] * Ws) + (pos >> 5), 1u << (pos & 31u));
         }
     }
     __syncwarp();
+    return hits;
 }
 
 // Number of DEPTH-vertex chains inside candidate set m of a single-word DAG.
@@ -94,9 +137,7 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
               u64 nverts, u64* next, u64 grab, u64* count) {
     __shared__ u32 sA[WPB][64];
     __shared__ __align__(8) u64 sR[WPB][64];
-    __shared__ u32 sEnd[WPB][32];
-    __shared__ __align__(8) u64 sOff[WPB][32];
-    __shared__ u32 sRow[WPB][32];
+    __shared__ __align__(8) u32 sScr[WPB][128];
     __shared__ u32 sHK[WPB][128];
     __shared__ u32 sHV[WPB][128];
     const u32 lane = g2m_lane();
@@ -116,14 +157,21 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
             const u32 d = (u32)(__ldg(off + u + 1) - b);
             A[lane] = lane < d ? __ldg(nbr + b + lane) : 0xffffffffu;
             A[lane + 32] = lane + 32 < d ? __ldg(nbr + b + lane + 32) : 0xffffffffu;
-            R[lane] = 0;
-            R[lane + 32] = 0;
+            if constexpr (K > 3) {
+                R[lane] = 0;
+                R[lane + 32] = 0;
+            }
             __syncwarp();
             const u32 hl = g2m_hlog(d);
             g2m_hmap_build(sHK[w], sHV[w], hl, A, d, lane, 32);
-            build_rows(off, nbr, A, d, 0, R, 1, sEnd[w], sOff[w], sRow[w], sHK[w], sHV[w], hl);
-            if (d > 32) build_rows(off, nbr, A, d, 32, R, 1, sEnd[w], sOff[w], sRow[w], sHK[w], sHV[w], hl);
-            for (u32 i = lane; i < d; i += 32) acc += Chain1<K - 2>::run(R, R[i]);
+            const HashProbe P{sHK[w], sHV[w], hl, A[0], A[d - 1]};
+            u32 h = probe_rows<K>(off, nbr, A, d, 0, R, 1, sScr[w], P);
+            if (d > 32) h += probe_rows<K>(off, nbr, A, d, 32, R, 1, sScr[w], P);
+            if constexpr (K == 3) {
+                acc += h;
+            } else {
+                for (u32 i = lane; i < d; i += 32) acc += Chain1<K - 2>::run(R, R[i]);
+            }
             __syncwarp();
         }
     }
@@ -149,39 +197,114 @@ __device__ __forceinline__ u32 compact_bits(const u64* words, u32 q0, u32 q1, u3
     return n;
 }
 
+// Per-warp scratch of the CTA tier (u32 words): L1[256] L2[256] (k > 3).
+__host__ __device__ constexpr u32 cta_warp_words(int K) { return K > 3 ? 512u : 0u; }
+
+// Shared-memory bytes of one CTA-tier block (layout in k_clique_cta).
+__host__ __device__ constexpr size_t cta_smem_bytes(int K, int W, int NW, u32 bmw) {
+    return (K > 3 ? (size_t)8 * (64 * W + NW) * (W + 1) : 0)   // R, T
+           + (size_t)8 * 64 * W                                  // RB
+           + (size_t)4 * 64 * W * 2 + (size_t)4 * 2 * W          // A, RE, BT
+           + (size_t)4 * 256 * W                                 // hash keys + vals
+           + (size_t)NW * 4 * cta_warp_words(K)                  // per-warp scratch
+           + (size_t)4 * bmw + (size_t)2 * ((bmw + 1) & ~1u);    // bitmap, pre
+}
+
+// CTA-wide flattened probe of all out-lists N+(A[i]), i < d: the warps
+// stride over the concatenation in 64-element steps (every warp gets the
+// same number of elements, whatever the row lengths). RE[i] is the
+// inclusive end of row i in the concatenation, RB[i] the nbr index of its
+// position 0. K == 3 counts members; otherwise sets the row bits of R.
+template <int K, int NW, typename Probe>
+__device__ __forceinline__ u32 cta_probe(const u32* __restrict__ nbr, const u32* RE, const u64* RB, u32 d,
+                                         u32 tot, u32 w, u64* R, u32 Ws, const Probe& P) {
+    const u32 lane = g2m_lane();
+    u32 hits = 0;
+    u32 o0 = 0;      // first row whose end is beyond the warp's first element (warp-uniform)
+    for (u32 e0 = w * 64; e0 < tot; e0 += NW * 64) {
+        for (;;) {   // RE is non-decreasing, so "RE[r] <= e0" holds on a prefix
+            const u32 r = o0 + lane;
+            const u32 n = __popc(__ballot_sync(G2M_FULL, r < d && RE[r] <= e0));
+            o0 += n;
+            if (n < 32) break;
+        }
+        const u32 ea = e0 + lane, eb = ea + 32;
+        u32 oa = o0, ob = o0;
+        u32 xa = 0, xb = 0;
+        if (ea < tot) {
+            while (RE[oa] <= ea) ++oa;
+            xa = __ldg(nbr + (RB[oa] + ea));
+        }
+        if (eb < tot) {
+            ob = oa;
+            while (RE[ob] <= eb) ++ob;
+            xb = __ldg(nbr + (RB[ob] + eb));
+        }
+        if constexpr (K == 3) {
+            hits += (ea < tot && P.has(xa)) ? 1u : 0u;
+            hits += (eb < tot && P.has(xb)) ? 1u : 0u;
+        } else {
+            if (ea < tot) {
+                const u32 pos = P.get(xa);
+                if (pos != G2M_EMPTY)   // 32-bit halves: native ATOMS.OR (64-bit would be a CAS loop)
+                    atomicOr((u32*)(R + (u64)oa * Ws) + (pos >> 5), 1u << (pos & 31u));
+            }
+            if (eb < tot) {
+                const u32 pos = P.get(xb);
+                if (pos != G2M_EMPTY)
+                    atomicOr((u32*)(R + (u64)ob * Ws) + (pos >> 5), 1u << (pos & 31u));
+            }
+        }
+    }
+    return hits;
+}
+
 // ---------------------------------------------------------------------------
 // CTA tier: 64 < d <= 64*W, one CTA of NW warps per source vertex, W-word
-// rows with an odd stride. Each warp takes rows i; the candidates j of R_i
-// are compacted (CH words at a time) into a shared list so every lane gets
-// a candidate. k=5: t2 = R_i & R_j stays in the lane's registers when small;
-// large ones are compacted again and shared by the whole warp.
+// rows with an odd stride. Local-graph construction is one CTA-wide
+// flattened pass over all out-lists (cta_probe); rows are counted in
+// dynamic single-row grabs, so the CTA barrier does not wait on the
+// unluckiest warp. The candidates j of R_i are compacted (CH words at a
+// time) into a shared list so every lane gets a candidate; R_j has no bits
+// below j (rank-space DAG), so only words >= j/64 are ANDed. k=5:
+// t2 = R_i & R_j stays in the lane's registers when small; large ones are
+// compacted again and shared by the whole warp.
+// bmw: u32 words of the window bitmap (0 = hash only).
 // ---------------------------------------------------------------------------
 template <int K, int W, int NW>
 __global__ void __launch_bounds__(NW * 32)
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-             u64 nverts, u64* next, u64* count) {
+             u64 nverts, u64* next, u64* count, u32 bmw) {
     constexpr u32 CH = 4;             // words compacted per round (<= 256 candidates)
     extern __shared__ __align__(16) u64 smem[];
-    // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64 | A [64W] u32 |
-    //         hash keys, vals [128W] u32 each | per-warp: end[32] row[32] off[32 u64] L1[256] L2[256]
+    // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64   (K > 3 only)
+    //         RB [64W] u64 | A [64W] u32 | RE [64W] u32 | BT [2W] u32
+    //         hash keys, vals [128W] u32 each | per-warp scratch | bitmap [bmw] u32 | pre [bmw] u16
     u64* R = smem;
-    u64* T = R + 64 * W * (W + 1);
-    u32* A = (u32*)(T + NW * (W + 1));
-    u32* HK = A + 64 * W;
+    u64* T = R + (K > 3 ? 64 * W * (W + 1) : 0);
+    u64* RB = T + (K > 3 ? NW * (W + 1) : 0);
+    u32* A = (u32*)(RB + 64 * W);
+    u32* RE = A + 64 * W;
+    u32* BT = RE + 64 * W;
+    u32* HK = BT + 2 * W;
     u32* HV = HK + 128 * W;
-    u32* base = HV + 128 * W;
+    u32* scr = HV + 128 * W;
+    u32* BM = scr + NW * cta_warp_words(K);
+    u16* PRE = (u16*)(BM + bmw);
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
-    u32* fl_end = base + w * 640;
-    u32* fl_row = fl_end + 32;
-    u64* fl_off = (u64*)(fl_end + 64);
-    u32* L1 = fl_end + 128;
+    u32* L1 = scr + w * cta_warp_words(K);
     u32* L2 = L1 + 256;
     u64* t2s = T + w * (W + 1);
     __shared__ u64 s_u;
+    __shared__ u32 s_cnt, s_tot;
+    for (u32 x = threadIdx.x; x < bmw; x += NW * 32) BM[x] = 0;
     u64 acc = 0;
     for (;;) {
-        if (threadIdx.x == 0) s_u = atomicAdd(next, 1ull);
+        if (threadIdx.x == 0) {
+            s_u = atomicAdd(next, 1ull);
+            s_cnt = 0;
+        }
         __syncthreads();
         const u64 t = s_u;
         if (t >= nverts) break;
@@ -190,93 +313,162 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         const u32 d = (u32)(__ldg(off + u + 1) - b);
         const u32 Wd = (d + 63) >> 6;
         const u32 Ws = Wd | 1u;          // odd row stride (bank spread)
-        for (u32 x = threadIdx.x; x < d; x += NW * 32) A[x] = __ldg(nbr + b + x);
-        for (u32 x = threadIdx.x; x < d * Ws; x += NW * 32) R[x] = 0;
-        __syncthreads();
-        const u32 hl = g2m_hlog(d);
-        g2m_hmap_build(HK, HV, hl, A, d, threadIdx.x, NW * 32);
-        for (u32 i0 = w * 32; i0 < d; i0 += NW * 32)
-            build_rows(off, nbr, A, d, i0, R, Ws, fl_end, fl_off, fl_row, HK, HV, hl);
-        __syncthreads();
-        for (u32 i = w; i < d; i += NW) {
-            const u64* Ri = R + (u64)i * Ws;
-            const u64 myw = lane < Wd ? Ri[lane] : 0ull;
-            if (K == 3) {
-                acc += (u64)__popcll(myw);
-                continue;
+        const u32 a0 = __ldg(nbr + b), alast = __ldg(nbr + b + d - 1);
+        const u32 span = alast - a0 + 1u;
+        const bool use_bm = span <= bmw * 32u;
+        // A, window bits, and per-32-row batches of the flattened out-lists
+        for (u32 bt = w; bt * 32 < d; bt += NW) {
+            const u32 i = bt * 32 + lane;
+            u64 ro = 0;
+            u32 rn = 0;
+            if (i < d) {
+                const u32 y = __ldg(nbr + b + i);
+                A[i] = y;
+                if (use_bm) {
+                    const u32 o = y - a0;
+                    atomicOr(BM + (o >> 5), 1u << (o & 31u));
+                    // first member of its word: local id base of that word
+                    if (i == 0 || ((__ldg(nbr + b + i - 1) - a0) >> 5) != (o >> 5)) PRE[o >> 5] = (u16)i;
+                }
+                ro = __ldg(off + y);
+                rn = (u32)(__ldg(off + y + 1) - ro);
+                // out-neighbours of y are > y >= A0; drop the tail beyond A_last
+                if (rn > 32 && __ldg(nbr + ro + rn - 1) > alast) rn = g2m_lb(nbr + ro, rn, alast + 1u);
             }
-            const u32 nzw = __ballot_sync(G2M_FULL, myw != 0ull);
-            if (!nzw) continue;
-            for (u32 c0 = 0; c0 < Wd; c0 += CH) {
-                if (!((nzw >> c0) & ((1u << CH) - 1u))) continue;
-                const u32 n1 = compact_bits(Ri, c0, min(c0 + CH, Wd), L1);
-                for (u32 e0 = 0; e0 < n1; e0 += 32) {
-                    const u32 e = e0 + lane;
-                    const bool isj = e < n1;
-                    const u32 j = isj ? L1[e] : 0u;
-                    const u64* Rj = R + (u64)j * Ws;
-                    if (K == 4) {
-                        if (isj) {
-                            u32 m = nzw;
-                            while (m) {
-                                const int q = __ffs(m) - 1;
-                                m &= m - 1;
-                                acc += (u64)__popcll(Ri[q] & Rj[q]);
-                            }
-                        }
-                    } else {   // K == 5
-                        u64 t2[W];
-                        u32 c = 0;
+            const u32 incl = g2m_scan_incl(rn);
+            if (i < d) {
+                RE[i] = incl;
+                RB[i] = ro - (u64)(incl - rn);
+            }
+            if (lane == 31) BT[bt] = incl;
+        }
+        if constexpr (K > 3)
+            for (u32 x = threadIdx.x; x < d * Ws; x += NW * 32) R[x] = 0;
+        __syncthreads();
+        u32 hl = 0;
+        if (!use_bm) {
+            hl = g2m_hlog(d);
+            g2m_hmap_build(HK, HV, hl, A, d, threadIdx.x, NW * 32);
+        }
+        if (w == 0) {   // batch offsets (<= 2W batches, 4 per lane)
+            const u32 nb = (d + 31) >> 5;
+            u32 v[4], sum = 0;
 #pragma unroll
-                        for (int r = 0; r < W; ++r) {
-                            t2[r] = (isj && r < (int)Wd) ? (Ri[r] & Rj[r]) : 0ull;
-                            c += (u32)__popcll(t2[r]);
-                        }
-                        const bool heavy = c > 32;
-                        if (isj && !heavy) {
+            for (int q = 0; q < 4; ++q) {
+                const u32 idx = lane * 4 + q;
+                v[q] = idx < nb ? BT[idx] : 0u;
+                sum += v[q];
+            }
+            const u32 incl = g2m_scan_incl(sum);
+            u32 ex = incl - sum;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const u32 idx = lane * 4 + q;
+                if (idx < nb) BT[idx] = ex;
+                ex += v[q];
+            }
+            if (lane == 31) s_tot = incl;
+        }
+        __syncthreads();
+        for (u32 x = threadIdx.x; x < d; x += NW * 32) {
+            const u32 bo = BT[x >> 5];
+            RE[x] += bo;
+            RB[x] -= bo;
+        }
+        __syncthreads();
+        // ---- build rows (K > 3) / count triangles (K == 3)
+        const u32 tot = s_tot;
+        u32 hits;
+        if (use_bm)
+            hits = cta_probe<K, NW>(nbr, RE, RB, d, tot, w, R, Ws, BitmapProbe{BM, PRE, a0, span});
+        else
+            hits = cta_probe<K, NW>(nbr, RE, RB, d, tot, w, R, Ws, HashProbe{HK, HV, hl, a0, alast});
+        if constexpr (K == 3) acc += hits;
+        __syncthreads();
+        if constexpr (K > 3) {
+            for (;;) {
+                u32 i = 0;
+                if (lane == 0) i = atomicAdd(&s_cnt, 1u);
+                i = __shfl_sync(G2M_FULL, i, 0);
+                if (i >= d) break;
+                const u64* Ri = R + (u64)i * Ws;
+                const u64 myw = lane < Wd ? Ri[lane] : 0ull;
+                const u32 nzw = __ballot_sync(G2M_FULL, myw != 0ull);
+                if (!nzw) continue;
+                for (u32 c0 = 0; c0 < Wd; c0 += CH) {
+                    if (!((nzw >> c0) & ((1u << CH) - 1u))) continue;
+                    const u32 n1 = compact_bits(Ri, c0, min(c0 + CH, Wd), L1);
+                    for (u32 e0 = 0; e0 < n1; e0 += 32) {
+                        const u32 e = e0 + lane;
+                        const bool isj = e < n1;
+                        const u32 j = isj ? L1[e] : 0u;
+                        const u64* Rj = R + (u64)j * Ws;
+                        if constexpr (K == 4) {
+                            if (isj) {
+                                u32 m = nzw & ~((1u << (j >> 6)) - 1u);   // R_j is zero below word j/64
+                                while (m) {
+                                    const int q = __ffs(m) - 1;
+                                    m &= m - 1;
+                                    acc += (u64)__popcll(Ri[q] & Rj[q]);
+                                }
+                            }
+                        } else {   // K == 5
+                            u64 t2[W];
+                            u32 c = 0;
 #pragma unroll
                             for (int r = 0; r < W; ++r) {
-                                u64 bits = t2[r];
-                                while (bits) {
-                                    const u32 l = r * 64 + (__ffsll(bits) - 1);
-                                    bits &= bits - 1;
-                                    const u64* Rl = R + (u64)l * Ws;
-#pragma unroll
-                                    for (int r2 = 0; r2 < W; ++r2)
-                                        if (t2[r2]) acc += (u64)__popcll(t2[r2] & Rl[r2]);
-                                }
+                                t2[r] = (isj && r < (int)Wd) ? (Ri[r] & Rj[r]) : 0ull;
+                                c += (u32)__popcll(t2[r]);
                             }
-                        }
-                        u32 hm = __ballot_sync(G2M_FULL, isj && heavy);
-                        while (hm) {
-                            const int hj = __ffs(hm) - 1;
-                            hm &= hm - 1;
-                            if ((int)lane == hj) {
+                            const bool heavy = c > 32;
+                            if (isj && !heavy) {
 #pragma unroll
-                                for (int r = 0; r < W; ++r) if (r < (int)Wd) t2s[r] = t2[r];
-                            }
-                            __syncwarp();
-                            const u32 nz2 = __ballot_sync(G2M_FULL, lane < Wd && t2s[lane < Wd ? lane : 0] != 0ull);
-                            for (u32 c2 = 0; c2 < Wd; c2 += CH) {
-                                if (!((nz2 >> c2) & ((1u << CH) - 1u))) continue;
-                                const u32 n2 = compact_bits(t2s, c2, min(c2 + CH, Wd), L2);
-                                for (u32 f = lane; f < n2; f += 32) {
-                                    const u64* Rl = R + (u64)L2[f] * Ws;
-                                    u32 m = nz2;
-                                    while (m) {
-                                        const int q3 = __ffs(m) - 1;
-                                        m &= m - 1;
-                                        acc += (u64)__popcll(t2s[q3] & Rl[q3]);
+                                for (int r = 0; r < W; ++r) {
+                                    u64 bits = t2[r];
+                                    while (bits) {
+                                        const u32 l = r * 64 + (__ffsll(bits) - 1);
+                                        bits &= bits - 1;
+                                        const u64* Rl = R + (u64)l * Ws;
+#pragma unroll
+                                        for (int r2 = 0; r2 < W; ++r2)
+                                            if (t2[r2]) acc += (u64)__popcll(t2[r2] & Rl[r2]);
                                     }
                                 }
+                            }
+                            u32 hm = __ballot_sync(G2M_FULL, isj && heavy);
+                            while (hm) {
+                                const int hj = __ffs(hm) - 1;
+                                hm &= hm - 1;
+                                if ((int)lane == hj) {
+#pragma unroll
+                                    for (int r = 0; r < W; ++r) if (r < (int)Wd) t2s[r] = t2[r];
+                                }
                                 __syncwarp();
+                                const u32 nz2 = __ballot_sync(G2M_FULL, lane < Wd && t2s[lane < Wd ? lane : 0] != 0ull);
+                                for (u32 c2 = 0; c2 < Wd; c2 += CH) {
+                                    if (!((nz2 >> c2) & ((1u << CH) - 1u))) continue;
+                                    const u32 n2 = compact_bits(t2s, c2, min(c2 + CH, Wd), L2);
+                                    for (u32 f = lane; f < n2; f += 32) {
+                                        const u64* Rl = R + (u64)L2[f] * Ws;
+                                        u32 m = nz2;
+                                        while (m) {
+                                            const int q3 = __ffs(m) - 1;
+                                            m &= m - 1;
+                                            acc += (u64)__popcll(t2s[q3] & Rl[q3]);
+                                        }
+                                    }
+                                    __syncwarp();
+                                }
                             }
                         }
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
+        // clear the window bits of this source (the bitmap stays all-zero between sources)
+        if (use_bm)
+            for (u32 x = threadIdx.x; x < d; x += NW * 32) BM[(A[x] - a0) >> 5] = 0;
         __syncthreads();
     }
     acc = g2m_wsum(acc);
@@ -284,23 +476,27 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
 }
 
 // Bucket the sources of this partition by local-graph size class.
-// class 0: d < K-1 (no clique), 1: d <= 64 (warp), 2..5: W = 2,4,8,16 (CTA),
-// 6: d > 1024 (generic kernel).
-__global__ void k_clique_bucket(const u64* off, u64 nv, int kmin1, u64 rr_chunk, u32 parts, u32 part,
-                                u32* lists, u64 list_stride, u64* sizes) {
+// class 0: d < K-1 (no clique), 1: d <= 64 (warp), 2..5: d <= 128..1024
+// (CTA, W = 2,4,8,16), 7: 1024 < d <= max_cta_d (CTA, W = 64; k = 3 only),
+// 6: d > max_cta_d (generic kernel). span_max[c]: widest id window of class c.
+__global__ void k_clique_bucket(const u64* off, const u32* nbr, u64 nv, int kmin1, u64 max_cta_d, u64 rr_chunk,
+                                u32 parts, u32 part, u32* lists, u64 list_stride, u64* sizes, u32* span_max) {
     for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x) {
         if (rr_chunk && ((v / rr_chunk) % parts) != part) continue;
-        const u64 d = off[v + 1] - off[v];
+        const u64 b = off[v];
+        const u64 d = off[v + 1] - b;
         int c;
-        if (d < (u64)kmin1) continue;
+        if (d < (u64)kmin1 || d == 0) continue;
         if (d <= 64) c = 1;
         else if (d <= 128) c = 2;
         else if (d <= 256) c = 3;
         else if (d <= 512) c = 4;
         else if (d <= 1024) c = 5;
+        else if (d <= max_cta_d) c = 7;
         else c = 6;
         const u64 slot = atomicAdd(sizes + c, 1ull);
         lists[(u64)c * list_stride + slot] = (u32)v;
+        if (c >= 2 && c != 6) atomicMax(span_max + c, __ldg(nbr + b + d - 1) - __ldg(nbr + b) + 1u);
     }
 }
 

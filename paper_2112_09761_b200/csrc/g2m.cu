@@ -182,6 +182,9 @@ struct g2m_graph {
     DevBuf red_off;          // reduced (src > dst) task offsets, lazily built
     uint64_t red_total = 0;
     bool has_red = false;
+    // oriented graphs: the same DAG relabelled by its (degree, id) order, lazily built
+    DevBuf rk_off, rk_nbr;
+    bool has_rank = false;
 };
 
 __global__ void k_max_degree(const u64* off, u64 nv, u64* out) {
@@ -519,6 +522,135 @@ static int ensure_reduced(const g2m_graph* cg, DevState* st) {
     G2M_CUDA(cudaMemcpyAsync(&g->red_total, g->red_off.as<u64>() + g->nv, 8, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     g->has_red = true;
+    return G2M_OK;
+}
+
+// ---- rank-space DAG (derived, oriented graphs only)
+//
+// The oriented graph keeps u->v iff (deg_u, u) < (deg_v, v) (graph.py:204-221).
+// Relabelling every vertex by its position in that order (its *rank*) turns
+// the DAG into "edges point to larger ids", with the high-degree vertices at
+// the top of the id range. Counts are invariant under the renaming
+// (SURVEY 7.3-3); what changes is locality: N+(u) of a source in the
+// bitmap-LGS tiers spans a narrow id window, so a direct-address bitmap of
+// that window in shared memory replaces hashing (clique_kernels.cuh).
+// deg_v = d+(v) + d-(v) on the oriented graph (each undirected edge is kept
+// once), so the order is recomputed exactly without the undirected graph.
+
+__global__ void k_rank_indeg(const u32* nbr, u64 slots, u32* indeg) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < slots; i += (u64)gridDim.x * blockDim.x)
+        atomicAdd(indeg + __ldg(nbr + i), 1u);
+}
+
+__global__ void k_rank_keys(const u64* off, const u32* indeg, u64 nv, u64* keys) {
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x)
+        keys[v] = ((off[v + 1] - off[v] + (u64)indeg[v]) << 32) | v;
+}
+
+__global__ void k_rank_scatter(const u64* off, const u64* sorted, u64 nv, u32* rank, u64* rdeg) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nv; i += (u64)gridDim.x * blockDim.x) {
+        const u32 v = (u32)sorted[i];
+        rank[v] = (u32)i;
+        rdeg[i] = off[v + 1] - off[v];
+    }
+}
+
+__global__ void k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* roff, u32* out) {
+    const u32 lane = g2m_lane();
+    for (u64 v = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; v < nv;
+         v += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u64 b = off[v], e = off[v + 1];
+        if (b == e) continue;
+        u32* dst = out + roff[rank[v]];
+        for (u64 i = b + lane; i < e; i += 32) dst[i - b] = __ldg(rank + __ldg(nbr + i));
+    }
+}
+
+__global__ void k_sub_base(const u64* in, u64 n, u64 base, i64* out) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        out[i] = (i64)(in[i] - base);
+}
+
+static int ensure_rank(const g2m_graph* cg, DevState* st) {
+    g2m_graph* g = const_cast<g2m_graph*>(cg);
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->has_rank) return G2M_OK;
+    if (!g->oriented) return fail(G2M_EUSAGE, "rank relabelling needs an oriented graph");
+    const u64 nv = g->nv, slots = g->slots;
+    G2M_TRY(g->rk_off.ensure((nv + 1) * 8));
+    G2M_TRY(g->rk_nbr.ensure(std::max<u64>(slots, 1) * 4));
+    DevBuf indeg, keys, sorted, rank, rdeg, tmp;
+    G2M_TRY(indeg.ensure(std::max<u64>(nv, 1) * 4));
+    G2M_TRY(keys.ensure(std::max<u64>(nv, 1) * 8));
+    G2M_TRY(sorted.ensure(std::max<u64>(nv, 1) * 8));
+    G2M_TRY(rank.ensure(std::max<u64>(nv, 1) * 4));
+    G2M_TRY(rdeg.ensure(std::max<u64>(nv, 1) * 8));
+    G2M_TRY(tmp.ensure(std::max<u64>(slots, 1) * 4));
+    G2M_CUDA(cudaMemsetAsync(indeg.p, 0, std::max<u64>(nv, 1) * 4, st->stream));
+    if (nv) {
+        if (slots) {
+            ++st->launches;
+            k_rank_indeg<<<grid_for(st, slots, 256), 256, 0, st->stream>>>(g->nbr.as<u32>(), slots, indeg.as<u32>());
+        }
+        ++st->launches;
+        k_rank_keys<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), indeg.as<u32>(), nv, keys.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+        int hi = 32;
+        while (hi < 64 && ((u64)1 << (hi - 32)) <= 2 * std::max<u64>(slots, 1)) ++hi;   // degree < 2^(hi-32)
+        size_t tb = 0;
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.as<u64>(), sorted.as<u64>(), (int64_t)nv, 0, hi,
+                                                st->stream));
+        G2M_TRY(st->cub_tmp.ensure(tb));
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(st->cub_tmp.p, tb, keys.as<u64>(), sorted.as<u64>(), (int64_t)nv, 0,
+                                                hi, st->stream));
+        ++st->launches;
+        k_rank_scatter<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), sorted.as<u64>(), nv,
+                                                                       rank.as<u32>(), rdeg.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_TRY(exclusive_scan_u64(st, rdeg.as<u64>(), g->rk_off.as<u64>(), nv));
+    if (nv && slots) {
+        ++st->launches;
+        k_rank_fill<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), nv,
+                                                                          rank.as<u32>(), g->rk_off.as<u64>(),
+                                                                          tmp.as<u32>());
+        G2M_CUDA(cudaGetLastError());
+        // sort every row; cub's segmented sort takes int item counts, so go in
+        // batches of whole rows with < 2^30 items (rows are <= max degree long)
+        std::vector<u64> hoff(nv + 1);
+        G2M_CUDA(cudaMemcpyAsync(hoff.data(), g->rk_off.p, (nv + 1) * 8, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        const u64 kBatch = (u64)1 << 30;
+        DevBuf rel;
+        G2M_TRY(rel.ensure((nv + 1) * 8));
+        u64 r0 = 0;
+        while (r0 < nv) {
+            u64 r1 = std::upper_bound(hoff.begin() + r0, hoff.end(), hoff[r0] + kBatch) - hoff.begin() - 1;
+            if (r1 <= r0) r1 = r0 + 1;
+            if (r1 > nv) r1 = nv;
+            const u64 base = hoff[r0], items = hoff[r1] - base;
+            if (items) {
+                // segment offsets relative to this batch
+                ++st->launches;
+                k_sub_base<<<grid_for(st, r1 - r0 + 1, 256), 256, 0, st->stream>>>(g->rk_off.as<u64>() + r0,
+                                                                                    r1 - r0 + 1, base, rel.as<i64>());
+                G2M_CUDA(cudaGetLastError());
+                const i64* bo = rel.as<i64>();
+                const i64* eo = rel.as<i64>() + 1;
+                size_t tb = 0;
+                G2M_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, tmp.as<u32>() + base,
+                                                            g->rk_nbr.as<u32>() + base, (int)items, (int)(r1 - r0),
+                                                            bo, eo, st->stream));
+                G2M_TRY(st->cub_tmp.ensure(tb));
+                G2M_CUDA(cub::DeviceSegmentedSort::SortKeys(st->cub_tmp.p, tb, tmp.as<u32>() + base,
+                                                            g->rk_nbr.as<u32>() + base, (int)items, (int)(r1 - r0),
+                                                            bo, eo, st->stream));
+            }
+            r0 = r1;
+        }
+    }
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    g->has_rank = true;
     return G2M_OK;
 }
 
@@ -955,15 +1087,18 @@ __global__ void k_heavy_fill(const u64* off, const u32* verts, u64 n, const u64*
     }
 }
 
+// Source classes of k_clique_bucket: 1 warp tier, 2..5 CTA tiers W = 2..16,
+// 7 CTA tier W = 64 (k = 3 only: no rows), 6 generic plan kernel.
+static const int kClasses = 8;
+
 template <int K>
-static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists, u64 stride,
-                             const uint64_t* sizes, u64* ctr, double* kms) {
+static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const u32* lists, u64 stride,
+                             const uint64_t* sizes, const uint32_t* spans, u64* ctr, double* kms) {
     using namespace g2m_clique;
-    const u64* off = g->off.as<u64>();
-    const u32* nbr = g->nbr.as<u32>();
     u64* count = ctr;        // (lo, hi)
     u64* next = ctr + 2;     // one work counter per launch
     int slot = 0;
+    const bool dbg = getenv("G2M_DEBUG") != nullptr;
     auto timed = [&](auto&& fn) -> int {
         G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
         fn();
@@ -973,6 +1108,7 @@ static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists,
         float ms = 0.f;
         cudaEventElapsedTime(&ms, st->ev0, st->ev1);
         *kms += ms;
+        if (dbg) fprintf(stderr, "[g2m]   launch %d: %.3f ms\n", slot, ms);
         return G2M_OK;
     };
     if (sizes[1]) {
@@ -985,30 +1121,44 @@ static int clique_launch_all(const g2m_graph* g, DevState* st, const u32* lists,
         }));
         ++slot;
     }
-    auto cta = [&](auto wtag, auto nwtag, int cls) -> int {
+    int max_smem = 0;
+    G2M_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+    int sm_smem = 0;
+    G2M_CUDA(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0));
+    auto cta = [&](auto wtag, auto nwtag, int cls, int want_ctas) -> int {
         constexpr int W = decltype(wtag)::value;
         constexpr int NW = decltype(nwtag)::value;
         if (!sizes[cls]) return G2M_OK;
-        const size_t smem = (size_t)8 * (64 * W + NW) * (W + 1) + (size_t)4 * 64 * W + (size_t)4 * 256 * W +
-                            (size_t)NW * 4 * 640;
+        // window bitmap: as wide as the widest source of the class needs, within
+        // the shared memory left at `want_ctas` blocks per SM
+        const size_t base = cta_smem_bytes(K, W, NW, 0);
+        const size_t per_block = std::min<size_t>((size_t)max_smem, (size_t)sm_smem / want_ctas - 1024);
+        u32 bmw = 0;
+        if (per_block > base + 64) bmw = (u32)std::min<size_t>((per_block - base) / 6, ((size_t)spans[cls] + 31) / 32);
+        bmw &= ~1u;
+        const size_t smem = cta_smem_bytes(K, W, NW, bmw);
         auto kern = k_clique_cta<K, W, NW>;
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
         G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
         const u64 grid = std::min<u64>(sizes[cls], (u64)st->sms * std::max(occ, 1));
+        if (dbg)
+            fprintf(stderr, "[g2m] clique k=%d class %d: %llu sources, W=%d NW=%d, window<=%u bits, bitmap %u bits, smem %zu, %d CTA/SM\n",
+                    K, cls, (unsigned long long)sizes[cls], W, NW, spans[cls], bmw * 32, smem, occ);
         G2M_TRY(timed([&] {
             ++st->launches;
             kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
-                                                                 next + slot, count);
+                                                                 next + slot, count, bmw);
         }));
         ++slot;
         return G2M_OK;
     };
     using std::integral_constant;
-    G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 4>{}, 2));
-    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 8>{}, 3));
-    G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, 4));
-    G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, 5));
+    G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 16>{}, 2, 2));
+    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, 3, 2));
+    G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, 4, 2));
+    G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, 5, 1));
+    if (K == 3) G2M_TRY(cta(integral_constant<int, 64>{}, integral_constant<int, 16>{}, 7, 1));
     return G2M_OK;
 }
 
@@ -1030,42 +1180,51 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     u64 rr_chunk = 0;
     u32 parts = 1, pt = 0;
     if (part && part->rr_chunk) {
+        if (part->rr_parts == 0) return fail(G2M_EUSAGE, "rr_parts must be positive");
         rr_chunk = part->rr_chunk;
         parts = part->rr_parts;
         pt = part->rr_part;
     }
-    // counters: ctr[8..9] count (lo, hi), ctr[10..] one work counter per launch
+    // the kernels run on the rank-space copy of the DAG (built once per graph)
+    G2M_TRY(ensure_rank(g, st));
+    const u64* off = g->rk_off.as<u64>();
+    const u32* nbr = g->rk_nbr.as<u32>();
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
+    // counters: ctr[8..9] count (lo, hi), ctr[10..] one work counter per launch
     G2M_TRY(st->counters.ensure(32 * 8));
     u64* ctr = st->counters.as<u64>();
-    // ctr[1], ctr[2]: count; work counters at ctr[8..]
     G2M_CUDA(cudaMemsetAsync(ctr, 0, 32 * 8, st->stream));
     const u64 stride = std::max<u64>(g->nv, 1);
-    G2M_TRY(st->tasks_b.ensure(7 * stride * 4));
-    G2M_TRY(st->tasks_a.ensure(8 * 8));
+    G2M_TRY(st->tasks_b.ensure((u64)kClasses * stride * 4));
+    G2M_TRY(st->tasks_a.ensure(kClasses * 8 + kClasses * 4));
     u64* dsizes = st->tasks_a.as<u64>();
-    G2M_CUDA(cudaMemsetAsync(dsizes, 0, 8 * 8, st->stream));
+    u32* dspans = (u32*)(dsizes + kClasses);
+    G2M_CUDA(cudaMemsetAsync(dsizes, 0, kClasses * 12, st->stream));
     if (g->nv) {
         ++st->launches;
         g2m_clique::k_clique_bucket<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(
-            g->off.as<u64>(), g->nv, k - 1, rr_chunk, parts, pt, st->tasks_b.as<u32>(), stride, dsizes);
+            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 1024, rr_chunk, parts, pt, st->tasks_b.as<u32>(), stride,
+            dsizes, dspans);
         G2M_CUDA(cudaGetLastError());
     }
-    uint64_t sizes[8];
-    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, 8 * 8, cudaMemcpyDeviceToHost, st->stream));
+    uint64_t sizes[kClasses];
+    uint32_t spans[kClasses];
+    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, kClasses * 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaMemcpyAsync(spans, dspans, kClasses * 4, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     const u32* lists = st->tasks_b.as<u32>();
     if (getenv("G2M_DEBUG"))
-        fprintf(stderr, "[g2m] clique k=%d buckets: skip<k-1 warp<=64:%llu 128:%llu 256:%llu 512:%llu 1024:%llu >1024:%llu\n",
+        fprintf(stderr, "[g2m] clique k=%d buckets: warp<=64:%llu 128:%llu 256:%llu 512:%llu 1024:%llu 4096:%llu generic:%llu\n",
                 k, (unsigned long long)sizes[1], (unsigned long long)sizes[2], (unsigned long long)sizes[3],
-                (unsigned long long)sizes[4], (unsigned long long)sizes[5], (unsigned long long)sizes[6]);
+                (unsigned long long)sizes[4], (unsigned long long)sizes[5], (unsigned long long)sizes[7],
+                (unsigned long long)sizes[6]);
     {
         u64* blk = ctr + 8;
         int rc;
         switch (k) {
-        case 3: rc = clique_launch_all<3>(g, st, lists, stride, sizes, blk, &S->kernel_ms); break;
-        case 4: rc = clique_launch_all<4>(g, st, lists, stride, sizes, blk, &S->kernel_ms); break;
-        default: rc = clique_launch_all<5>(g, st, lists, stride, sizes, blk, &S->kernel_ms); break;
+        case 3: rc = clique_launch_all<3>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms); break;
+        case 4: rc = clique_launch_all<4>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms); break;
+        default: rc = clique_launch_all<5>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms); break;
         }
         if (rc != G2M_OK) return rc;
     }
@@ -1073,16 +1232,17 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     G2M_CUDA(cudaMemcpyAsync(h, ctr + 8, 16, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     unsigned __int128 total = ((unsigned __int128)h[1] << 64) | h[0];
-    S->tasks = sizes[1] + sizes[2] + sizes[3] + sizes[4] + sizes[5] + sizes[6];
+    S->tasks = 0;
+    for (int c = 1; c < kClasses; ++c) S->tasks += sizes[c];
     // sources beyond the bitmap tiers: the generated plan kernel over their edge tasks
     if (sizes[6]) {
-        if (!fallback) return fail(G2M_EUSAGE, "sources with out-degree > 1024 need a fallback kernel");
+        if (!fallback) return fail(G2M_EUSAGE, "sources beyond the bitmap tiers need a fallback kernel");
         const u64 nh = sizes[6];
         DevBuf lens, pos, idx;
         G2M_TRY(lens.ensure(nh * 8));
         G2M_TRY(pos.ensure((nh + 1) * 8));
         ++st->launches;
-        k_heavy_len<<<grid_for(st, nh, 256), 256, 0, st->stream>>>(g->off.as<u64>(), lists + 6 * stride, nh, lens.as<u64>());
+        k_heavy_len<<<grid_for(st, nh, 256), 256, 0, st->stream>>>(off, lists + 6 * stride, nh, lens.as<u64>());
         G2M_CUDA(cudaGetLastError());
         G2M_TRY(exclusive_scan_u64(st, lens.as<u64>(), pos.as<u64>(), nh));
         uint64_t ntask = 0;
@@ -1090,18 +1250,18 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
         G2M_CUDA(cudaStreamSynchronize(st->stream));
         G2M_TRY(idx.ensure(std::max<uint64_t>(ntask, 1) * 8));
         ++st->launches;
-        k_heavy_fill<<<grid_for(st, nh * 32, 256), 256, 0, st->stream>>>(g->off.as<u64>(), lists + 6 * stride, nh,
+        k_heavy_fill<<<grid_for(st, nh * 32, 256), 256, 0, st->stream>>>(off, lists + 6 * stride, nh,
                                                                           pos.as<u64>(), idx.as<u64>());
         G2M_CUDA(cudaGetLastError());
         G2M_TRY(reset_counters(fallback, st));
         G2MArgs a;
         std::memset(&a, 0, sizeof(a));
-        a.off = g->off.as<u64>();
-        a.nbr = g->nbr.as<u32>();
+        a.off = off;
+        a.nbr = nbr;
         a.nv = g->nv;
         a.kind = G2M_TASKS_EDGE;
         a.source = G2M_SRC_INDEX;
-        a.task_off = g->off.as<u64>();
+        a.task_off = off;
         a.total_implicit = g->slots;
         a.t_index = idx.as<u64>();
         a.ntasks = ntask;

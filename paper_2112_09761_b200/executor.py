@@ -253,10 +253,11 @@ def _counts_from(words: np.ndarray, pids) -> dict[str, int]:
     return out
 
 
-# k values routed to the bitmap local-graph clique kernels (g2m_clique_count)
-LGS_CLIQUE_K = {4, 5}
-if os.environ.get("G2M_TC_LGS") == "1":
-    LGS_CLIQUE_K.add(3)
+# k values routed to the bitmap local-graph clique kernels (g2m_clique_count);
+# G2M_TC_LGS=0 sends triangle counting to the generated plan kernel instead
+LGS_CLIQUE_K = {3, 4, 5}
+if os.environ.get("G2M_TC_LGS") == "0":
+    LGS_CLIQUE_K.discard(3)
 
 
 def _lgs_clique_k(g: Graph, forest: PlanForest, tasks, sink, index) -> int:
