@@ -200,9 +200,15 @@ __device__ __forceinline__ u32 compact_bits(const u64* words, u32 q0, u32 q1, u3
 // Per-warp scratch of the CTA tier (u32 words): L1[256] L2[256] (k > 3).
 __host__ __device__ constexpr u32 cta_warp_words(int K) { return K > 3 ? 512u : 0u; }
 
-// Shared-memory bytes of one CTA-tier block (layout in k_clique_cta).
-__host__ __device__ constexpr size_t cta_smem_bytes(int K, int W, int NW, u32 bmw) {
-    return (K > 3 ? (size_t)8 * (64 * W + NW) * (W + 1) : 0)   // R, T
+// u64 words of the local-graph rows R and the per-warp row buffers T.
+__host__ __device__ constexpr size_t cta_row_words(int K, int W, int NW) {
+    return K > 3 ? (size_t)(64 * W + NW) * (W + 1) : 0;
+}
+
+// Shared-memory bytes of one CTA-tier block (layout in k_clique_cta); with
+// GR the rows live in a global (L2-resident) slab per block instead.
+__host__ __device__ constexpr size_t cta_smem_bytes(int K, int W, int NW, u32 bmw, bool GR = false) {
+    return (GR ? 0 : (size_t)8 * cta_row_words(K, W, NW))        // R, T
            + (size_t)8 * 64 * W                                  // RB
            + (size_t)4 * 64 * W * 2 + (size_t)4 * 2 * W          // A, RE, BT
            + (size_t)4 * 256 * W                                 // hash keys + vals
@@ -271,18 +277,18 @@ __device__ __forceinline__ u32 cta_probe(const u32* __restrict__ nbr, const u32*
 // compacted again and shared by the whole warp.
 // bmw: u32 words of the window bitmap (0 = hash only).
 // ---------------------------------------------------------------------------
-template <int K, int W, int NW>
+template <int K, int W, int NW, bool GR = false>
 __global__ void __launch_bounds__(NW * 32)
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-             u64 nverts, u64* next, u64* count, u32 bmw) {
+             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows) {
     constexpr u32 CH = 4;             // words compacted per round (<= 256 candidates)
     extern __shared__ __align__(16) u64 smem[];
     // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64   (K > 3 only)
     //         RB [64W] u64 | A [64W] u32 | RE [64W] u32 | BT [2W] u32
     //         hash keys, vals [128W] u32 each | per-warp scratch | bitmap [bmw] u32 | pre [bmw] u16
-    u64* R = smem;
+    u64* R = GR ? grows + (u64)blockIdx.x * cta_row_words(K, W, NW) : smem;
     u64* T = R + (K > 3 ? 64 * W * (W + 1) : 0);
-    u64* RB = T + (K > 3 ? NW * (W + 1) : 0);
+    u64* RB = GR ? smem : T + (K > 3 ? NW * (W + 1) : 0);
     u32* A = (u32*)(RB + 64 * W);
     u32* RE = A + 64 * W;
     u32* BT = RE + 64 * W;
@@ -395,6 +401,38 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                 const u64 myw = lane < Wd ? Ri[lane] : 0ull;
                 const u32 nzw = __ballot_sync(G2M_FULL, myw != 0ull);
                 if (!nzw) continue;
+                if constexpr (K == 5) {
+                    // 4-cliques with local source i = triangles of the sub-DAG on
+                    // R_i. With n1 = |R_i| <= 64 its rows are single words:
+                    // S_k bit m <=> L1[m] in R_{L1[k]}, one ballot pair per k.
+                    const u32 n1 = __reduce_add_sync(G2M_FULL, (u32)__popcll(myw));
+                    if (n1 <= 64) {
+                        compact_bits(Ri, 0, Wd, L1);
+                        u64* SS = (u64*)L2;
+                        const u32 c0 = lane < n1 ? L1[lane] : 0u;
+                        const u32 c1 = lane + 32 < n1 ? L1[lane + 32] : 0u;
+                        for (u32 k = 0; k < n1; ++k) {
+                            const u64* Rk = R + (u64)L1[k] * Ws;   // no bits at or below L1[k]
+                            const bool b0 = lane < n1 && ((Rk[c0 >> 6] >> (c0 & 63u)) & 1ull);
+                            const bool b1 = lane + 32 < n1 && ((Rk[c1 >> 6] >> (c1 & 63u)) & 1ull);
+                            const u32 s0 = __ballot_sync(G2M_FULL, b0);
+                            const u32 s1 = __ballot_sync(G2M_FULL, b1);
+                            if (lane == 0) SS[k] = ((u64)s1 << 32) | s0;
+                        }
+                        __syncwarp();
+                        for (u32 k = lane; k < n1; k += 32) {
+                            const u64 Sk = SS[k];
+                            u64 it = Sk;
+                            while (it) {
+                                const int l = __ffsll(it) - 1;
+                                it &= it - 1;
+                                acc += (u64)__popcll(Sk & SS[l]);
+                            }
+                        }
+                        __syncwarp();
+                        continue;
+                    }
+                }
                 for (u32 c0 = 0; c0 < Wd; c0 += CH) {
                     if (!((nzw >> c0) & ((1u << CH) - 1u))) continue;
                     const u32 n1 = compact_bits(Ri, c0, min(c0 + CH, Wd), L1);
@@ -412,12 +450,12 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                                     acc += (u64)__popcll(Ri[q] & Rj[q]);
                                 }
                             }
-                        } else {   // K == 5
+                        } else {   // K == 5, rows with |R_i| > 64
                             u64 t2[W];
                             u32 c = 0;
 #pragma unroll
                             for (int r = 0; r < W; ++r) {
-                                t2[r] = (isj && r < (int)Wd) ? (Ri[r] & Rj[r]) : 0ull;
+                                t2[r] = (isj && r < (int)Wd && r >= (int)(j >> 6)) ? (Ri[r] & Rj[r]) : 0ull;
                                 c += (u32)__popcll(t2[r]);
                             }
                             const bool heavy = c > 32;
@@ -429,9 +467,10 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                                         const u32 l = r * 64 + (__ffsll(bits) - 1);
                                         bits &= bits - 1;
                                         const u64* Rl = R + (u64)l * Ws;
+                                        const int lw = (int)(l >> 6);   // R_l is zero below word l/64
 #pragma unroll
                                         for (int r2 = 0; r2 < W; ++r2)
-                                            if (t2[r2]) acc += (u64)__popcll(t2[r2] & Rl[r2]);
+                                            if (r2 >= lw && t2[r2]) acc += (u64)__popcll(t2[r2] & Rl[r2]);
                                     }
                                 }
                             }
@@ -449,8 +488,9 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                                     if (!((nz2 >> c2) & ((1u << CH) - 1u))) continue;
                                     const u32 n2 = compact_bits(t2s, c2, min(c2 + CH, Wd), L2);
                                     for (u32 f = lane; f < n2; f += 32) {
-                                        const u64* Rl = R + (u64)L2[f] * Ws;
-                                        u32 m = nz2;
+                                        const u32 l = L2[f];
+                                        const u64* Rl = R + (u64)l * Ws;
+                                        u32 m = nz2 & ~((1u << (l >> 6)) - 1u);   // R_l is zero below word l/64
                                         while (m) {
                                             const int q3 = __ffs(m) - 1;
                                             m &= m - 1;

@@ -1125,40 +1125,51 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     G2M_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
     int sm_smem = 0;
     G2M_CUDA(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0));
-    auto cta = [&](auto wtag, auto nwtag, int cls, int want_ctas) -> int {
+    DevBuf slab;   // global rows of the GR tier
+    auto cta = [&](auto wtag, auto nwtag, auto grtag, int cls, int want_ctas) -> int {
         constexpr int W = decltype(wtag)::value;
         constexpr int NW = decltype(nwtag)::value;
+        constexpr bool GR = decltype(grtag)::value;
         if (!sizes[cls]) return G2M_OK;
         // window bitmap: as wide as the widest source of the class needs, within
         // the shared memory left at `want_ctas` blocks per SM
-        const size_t base = cta_smem_bytes(K, W, NW, 0);
+        const size_t base = cta_smem_bytes(K, W, NW, 0, GR);
         const size_t per_block = std::min<size_t>((size_t)max_smem, (size_t)sm_smem / want_ctas - 1024);
         u32 bmw = 0;
         if (per_block > base + 64) bmw = (u32)std::min<size_t>((per_block - base) / 6, ((size_t)spans[cls] + 31) / 32);
         bmw &= ~1u;
-        const size_t smem = cta_smem_bytes(K, W, NW, bmw);
-        auto kern = k_clique_cta<K, W, NW>;
+        const size_t smem = cta_smem_bytes(K, W, NW, bmw, GR);
+        auto kern = k_clique_cta<K, W, NW, GR>;
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
         G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
         const u64 grid = std::min<u64>(sizes[cls], (u64)st->sms * std::max(occ, 1));
+        u64* grows = nullptr;
+        if (GR) {
+            G2M_TRY(slab.ensure(grid * cta_row_words(K, W, NW) * 8));
+            grows = slab.as<u64>();
+        }
         if (dbg)
-            fprintf(stderr, "[g2m] clique k=%d class %d: %llu sources, W=%d NW=%d, window<=%u bits, bitmap %u bits, smem %zu, %d CTA/SM\n",
-                    K, cls, (unsigned long long)sizes[cls], W, NW, spans[cls], bmw * 32, smem, occ);
+            fprintf(stderr, "[g2m] clique k=%d class %d: %llu sources, W=%d NW=%d%s, window<=%u bits, bitmap %u bits, smem %zu, %d CTA/SM\n",
+                    K, cls, (unsigned long long)sizes[cls], W, NW, GR ? " (rows in L2)" : "", spans[cls], bmw * 32, smem, occ);
         G2M_TRY(timed([&] {
             ++st->launches;
             kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
-                                                                 next + slot, count, bmw);
+                                                                 next + slot, count, bmw, grows);
         }));
         ++slot;
         return G2M_OK;
     };
     using std::integral_constant;
-    G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 16>{}, 2, 2));
-    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, 3, 2));
-    G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, 4, 2));
-    G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, 5, 1));
-    if (K == 3) G2M_TRY(cta(integral_constant<int, 64>{}, integral_constant<int, 16>{}, 7, 1));
+    using F = std::false_type;
+    G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 16>{}, F{}, 2, 2));
+    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, F{}, 3, 2));
+    G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, F{}, 4, 2));
+    G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, F{}, 5, 1));
+    if constexpr (K == 3)
+        G2M_TRY(cta(integral_constant<int, 64>{}, integral_constant<int, 16>{}, F{}, 7, 1));
+    else
+        G2M_TRY(cta(integral_constant<int, 32>{}, integral_constant<int, 16>{}, std::true_type{}, 7, 1));
     return G2M_OK;
 }
 
@@ -1203,7 +1214,7 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     if (g->nv) {
         ++st->launches;
         g2m_clique::k_clique_bucket<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(
-            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 1024, rr_chunk, parts, pt, st->tasks_b.as<u32>(), stride,
+            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 2048, rr_chunk, parts, pt, st->tasks_b.as<u32>(), stride,
             dsizes, dspans);
         G2M_CUDA(cudaGetLastError());
     }

@@ -338,12 +338,13 @@ def test_instrumented_bytes_match_oracle_rmat11(workload):
     assert EX.algorithmic_bytes(gd, forest) == want
 
 
-def _heavy_source_graph():
-    """A source u with out-degree 1100 (> the 1024 bitmap tier): u links to A
-    (1100 vertices); each a in A gets 1101 private leaves so deg(a) > deg(u);
-    A is internally an ER graph so cliques through u exist."""
+def _heavy_source_graph(na=1100):
+    """A source u with out-degree na (1100: the W=32/64 tiers; 2100: beyond
+    them, the generic fallback for k > 3): u links to A (na vertices); each a
+    in A gets na+1 private leaves so deg(a) > deg(u); A is internally an ER
+    graph so cliques through u exist."""
     rng = np.random.default_rng(11)
-    na, leaves = 1100, 1101
+    leaves = na + 1
     A = np.arange(1, na + 1)
     edges = [np.column_stack([np.zeros(na, dtype=np.int64), A])]
     mask = np.triu(rng.random((na, na)) < 0.02, 1)
@@ -362,7 +363,7 @@ def test_lgs_clique_kernels_match_generic_and_oracle(k):
     graphs = [complete(9), complete(70), er(200, 0.08, 21), er(150, 0.3, 5),
               GR.from_edges(G.rmat_edges(12, 16, 1), num_vertices=1 << 12),
               GR.from_edges(G.rmat_edges(14, 16, 3), num_vertices=1 << 14),
-              _heavy_source_graph()]
+              _heavy_source_graph(), _heavy_source_graph(2100)]
     for g in graphs:
         og = GR.orient(g)
         pl = make_plan(P.generate_clique(k), g, oriented=True)
@@ -377,6 +378,9 @@ def test_lgs_clique_kernels_match_generic_and_oracle(k):
     assert pm.k_clique(complete(70), 5).counts["5-clique"] == comb(70, 5)
     assert pm.k_clique(complete(64), 4).counts["4-clique"] == comb(64, 4)
     assert pm.k_clique(complete(65), 4).counts["4-clique"] == comb(65, 4)
+    big = complete(1200)      # out-degrees 0..1199: every tier incl. W=32/64
+    for kk in (3, 4, 5):
+        assert list(pm.k_clique(big, kk).counts.values()) == [comb(1200, kk)]
 
 
 def test_rmat12_lgs_known_counts():
