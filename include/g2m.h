@@ -31,6 +31,9 @@
  *                            produced on the device in exact reference
  *                            order (task order, then DFS order) and handed
  *                            to the host in batches (executor.py:275-280).
+ *   g2m_cycle4_count        run_dfs for the count-mode 4-cycle plan
+ *                            (executor.py:339-408 over plan.py:110-174):
+ *                            same count, wedge-aggregation kernels.
  *   g2m_setop_batch         setops.intersect/intersect_count/difference/
  *                            difference_count (setops.py:35-84) as a
  *                            batched device call (kernel-library parity).
@@ -182,6 +185,15 @@ int g2m_list(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* tasks
  * plan, over their edge tasks. counts_lo_hi receives (lo, hi). */
 int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
                      const g2m_kernel* fallback, const g2m_run_config* cfg,
+                     uint64_t* counts_lo_hi, g2m_run_stats* stats);
+
+/* 4-cycle count of a SYMMETRIC (unoriented) graph: the count-mode result of
+ * subgraph_listing(g, 4-cycle) (apps.py:291-297; plan PAPER.md §A.2),
+ * computed by wedge aggregation on the (degree, id) rank relabelling
+ * (cycle4_kernels.cuh). `part` (optional, IMPLICIT with rr_chunk/rr_parts/
+ * rr_part) restricts the highest-ranked cycle vertex to a chunked round-robin
+ * share. counts_lo_hi receives (lo, hi). */
+int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, const g2m_run_config* cfg,
                      uint64_t* counts_lo_hi, g2m_run_stats* stats);
 
 /* Batched sorted-set kernels (setops.py:35-84). Lists are concatenated u32

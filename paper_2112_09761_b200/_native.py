@@ -97,6 +97,8 @@ SIGNATURES = {
                            C.c_void_p, _u64p, C.POINTER(RunStats)]),
     "g2m_clique_count": (C.c_int, [_P, C.c_int32, C.POINTER(TaskSpec), _P, C.POINTER(RunConfig),
                                    _u64p, C.POINTER(RunStats)]),
+    "g2m_cycle4_count": (C.c_int, [_P, C.POINTER(TaskSpec), C.POINTER(RunConfig), _u64p,
+                                   C.POINTER(RunStats)]),
     "g2m_setop_batch": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _u32p, _u64p, _u32p,
                                   _u64p, _i64p, _u64p, _u32p]),
 }

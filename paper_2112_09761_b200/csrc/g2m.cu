@@ -7,6 +7,7 @@
 #include "g2m.h"
 #include "g2m_device.cuh"
 #include "clique_kernels.cuh"
+#include "cycle4_kernels.cuh"
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -131,6 +132,11 @@ struct DevBuf {
         bytes = n;
         return G2M_OK;
     }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
     template <typename T>
     T* as() const { return reinterpret_cast<T*>(p); }
 };
@@ -145,6 +151,8 @@ struct DevState {
     DevBuf tasks_a, tasks_b, task_match, matches, cub_tmp;
     int sms = 0;
     uint64_t launches = 0;   // kernels of ours launched on this device (g2m_run_stats.launches)
+    DevBuf c4slab;           // zeroed dense 4-cycle counters, one n-word slab per block
+    uint64_t c4slab_words = 0, c4slab_blocks = 0;
 };
 
 static std::mutex g_dev_mu;
@@ -182,7 +190,7 @@ struct g2m_graph {
     DevBuf red_off;          // reduced (src > dst) task offsets, lazily built
     uint64_t red_total = 0;
     bool has_red = false;
-    // oriented graphs: the same DAG relabelled by its (degree, id) order, lazily built
+    // the same graph relabelled by its (degree, id) order, lazily built
     DevBuf rk_off, rk_nbr;
     bool has_rank = false;
 };
@@ -536,6 +544,8 @@ static int ensure_reduced(const g2m_graph* cg, DevState* st) {
 // that window in shared memory replaces hashing (clique_kernels.cuh).
 // deg_v = d+(v) + d-(v) on the oriented graph (each undirected edge is kept
 // once), so the order is recomputed exactly without the undirected graph.
+// Symmetric graphs get the same relabelling with deg_v = row length
+// (cycle4_kernels.cuh).
 
 __global__ void k_rank_indeg(const u32* nbr, u64 slots, u32* indeg) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < slots; i += (u64)gridDim.x * blockDim.x)
@@ -575,7 +585,6 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     g2m_graph* g = const_cast<g2m_graph*>(cg);
     std::lock_guard<std::mutex> lk(g->mu);
     if (g->has_rank) return G2M_OK;
-    if (!g->oriented) return fail(G2M_EUSAGE, "rank relabelling needs an oriented graph");
     const u64 nv = g->nv, slots = g->slots;
     G2M_TRY(g->rk_off.ensure((nv + 1) * 8));
     G2M_TRY(g->rk_nbr.ensure(std::max<u64>(slots, 1) * 4));
@@ -588,7 +597,7 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     G2M_TRY(tmp.ensure(std::max<u64>(slots, 1) * 4));
     G2M_CUDA(cudaMemsetAsync(indeg.p, 0, std::max<u64>(nv, 1) * 4, st->stream));
     if (nv) {
-        if (slots) {
+        if (slots && g->oriented) {   // symmetric graphs: deg = row length, no in-degree term
             ++st->launches;
             k_rank_indeg<<<grid_for(st, slots, 256), 256, 0, st->stream>>>(g->nbr.as<u32>(), slots, indeg.as<u32>());
         }
@@ -1285,6 +1294,161 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     counts[1] = (uint64_t)(total >> 64);
     G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
     G2M_CUDA(cudaEventSynchronize(st->evs1));
+    float dm = 0.f;
+    cudaEventElapsedTime(&dm, st->evs0, st->evs1);
+    S->device_ms = dm;
+    S->launches = st->launches - l0;
+    S->total_ms = ms_since(t0);
+    return G2M_OK;
+}
+
+// ---------------------------------------------------------------------------
+// 4-cycle count by wedge aggregation (cycle4_kernels.cuh)
+// ---------------------------------------------------------------------------
+
+extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, const g2m_run_config* cfg,
+                                uint64_t* counts, g2m_run_stats* stats) {
+    (void)cfg;
+    if (!g || !counts) return fail(G2M_EUSAGE, "null argument");
+    if (g->oriented) return fail(G2M_EUSAGE, "plan orientation does not match the graph");
+    auto t0 = Clock::now();
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    g2m_run_stats local{};
+    g2m_run_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    const uint64_t l0 = st->launches;
+    u64 rr_chunk = 0;
+    u32 parts = 1, pt = 0;
+    if (part && part->rr_chunk) {
+        if (part->rr_parts == 0) return fail(G2M_EUSAGE, "rr_parts must be positive");
+        rr_chunk = part->rr_chunk;
+        parts = part->rr_parts;
+        pt = part->rr_part;
+    }
+    G2M_TRY(ensure_rank(g, st));
+    const u64* off = g->rk_off.as<u64>();
+    const u32* nbr = g->rk_nbr.as<u32>();
+    const u64 nv = g->nv;
+    const bool dbg = getenv("G2M_DEBUG") != nullptr;
+    G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
+    G2M_TRY(st->counters.ensure(32 * 8));
+    u64* ctr = st->counters.as<u64>();
+    G2M_CUDA(cudaMemsetAsync(ctr, 0, 32 * 8, st->stream));
+    const u64 stride = std::max<u64>(nv, 1);
+    // lists/lows: 4 classes x nv u32 each; wkeys (class 3 sort keys) 2 x nv u64
+    G2M_TRY(st->tasks_b.ensure(8 * stride * 4));
+    G2M_TRY(st->matches.ensure(2 * stride * 8));
+    G2M_TRY(st->tasks_a.ensure(4 * 8));
+    u32* lists = st->tasks_b.as<u32>();
+    u32* lows = lists + 4 * stride;
+    u64* wkeys = st->matches.as<u64>();
+    u64* wsorted = wkeys + stride;
+    u64* dsizes = st->tasks_a.as<u64>();
+    G2M_CUDA(cudaMemsetAsync(dsizes, 0, 4 * 8, st->stream));
+    if (nv) {
+        ++st->launches;
+        g2m_c4::k_c4_bucket<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(
+            off, nbr, nv, rr_chunk, parts, pt, lists, lows, wkeys, stride, dsizes);
+        G2M_CUDA(cudaGetLastError());
+    }
+    uint64_t sizes[4];
+    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, 4 * 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    if (dbg)
+        fprintf(stderr, "[g2m] cycle4: warp %llu, cta %llu, dense %llu sources\n", (unsigned long long)sizes[1],
+                (unsigned long long)sizes[2], (unsigned long long)sizes[3]);
+    // the dense tier runs its largest wedge fans first
+    if (sizes[3]) {
+        size_t tb = 0;
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, wkeys, wsorted, (int64_t)sizes[3], 0, 64, st->stream));
+        G2M_TRY(st->cub_tmp.ensure(tb));
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(st->cub_tmp.p, tb, wkeys, wsorted, (int64_t)sizes[3], 0, 64,
+                                                st->stream));
+        ++st->launches;
+        g2m_c4::k_c4_unpack<<<grid_for(st, sizes[3], 256), 256, 0, st->stream>>>(
+            wsorted, sizes[3], off, nbr, lists + 3 * stride, lows + 3 * stride);
+        G2M_CUDA(cudaGetLastError());
+    }
+    u64* count = ctr + 8;
+    u64* next = ctr + 10;
+    int slot = 0;
+    auto timed = [&](auto&& fn) -> int {
+        G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
+        fn();
+        G2M_CUDA(cudaGetLastError());
+        G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
+        G2M_CUDA(cudaEventSynchronize(st->ev1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, st->ev0, st->ev1);
+        S->kernel_ms += ms;
+        if (dbg) fprintf(stderr, "[g2m]   cycle4 launch %d: %.3f ms\n", slot, ms);
+        ++slot;
+        return G2M_OK;
+    };
+    if (sizes[1]) {
+        constexpr int WPB = 4;     // 4 x 8.4 KB of static shared memory
+        auto kern = g2m_c4::k_c4_warp<WPB>;
+        int occ = 0;
+        G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WPB * 32, 0));
+        G2M_TRY(timed([&] {
+            ++st->launches;
+            kern<<<st->sms * std::max(occ, 1), WPB * 32, 0, st->stream>>>(off, nbr, lists + stride, lows + stride,
+                                                                           sizes[1], next + 0, count);
+        }));
+    }
+    constexpr int NW = 16;
+    if (sizes[2]) {
+        const u32 cap = 16384;
+        const size_t smem = (size_t)2 * cap * 4 + (size_t)NW * 96 * 4;
+        auto kern = g2m_c4::k_c4_cta<NW, false>;
+        G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
+        const u64 grid = std::min<u64>(sizes[2], (u64)st->sms * std::max(occ, 1));
+        G2M_TRY(timed([&] {
+            ++st->launches;
+            kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + 2 * stride, lows + 2 * stride,
+                                                                 sizes[2], next + 1, count, nullptr, 0, cap);
+        }));
+    }
+    if (sizes[3]) {
+        const size_t smem = (size_t)NW * 96 * 4;
+        auto kern = g2m_c4::k_c4_cta<NW, true>;
+        int occ = 0;
+        G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
+        // one zeroed n-word counter slab per block, kept (zeroed) across calls,
+        // at most a quarter of the free HBM
+        u64 want = std::min<u64>(sizes[3], (u64)st->sms * std::max(occ, 1));
+        if (st->c4slab_words != stride || st->c4slab_blocks < want) {
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            const u64 nb = std::min<u64>(want, std::max<u64>(1, (fr + st->c4slab.bytes) / 4 / (stride * 4)));
+            if (st->c4slab_words != stride || nb > st->c4slab_blocks) {
+                st->c4slab.release();
+                G2M_TRY(st->c4slab.ensure(nb * stride * 4));
+                G2M_CUDA(cudaMemsetAsync(st->c4slab.p, 0, nb * stride * 4, st->stream));
+                st->c4slab_words = stride;
+                st->c4slab_blocks = nb;
+            }
+        }
+        const u64 grid = std::min<u64>(want, st->c4slab_blocks);
+        G2M_TRY(timed([&] {
+            ++st->launches;
+            kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + 3 * stride, lows + 3 * stride,
+                                                                 sizes[3], next + 2, count, st->c4slab.as<u32>(),
+                                                                 stride, 0);
+        }));
+    }
+    uint64_t h[2] = {0, 0};
+    G2M_CUDA(cudaMemcpyAsync(h, count, 16, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
+    G2M_CUDA(cudaEventSynchronize(st->evs1));
+    counts[0] = h[0];
+    counts[1] = h[1];
+    S->tasks = sizes[1] + sizes[2] + sizes[3];
     float dm = 0.f;
     cudaEventElapsedTime(&dm, st->evs0, st->evs1);
     S->device_ms = dm;

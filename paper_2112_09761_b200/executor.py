@@ -24,6 +24,7 @@ import numpy as np
 from . import _native as N
 from . import codegen
 from .graph import EdgeTaskList, Graph, build_edge_tasks
+from .pattern import EDGE_INDUCED
 from .plan import (EDGE_PARALLEL, EMIT_MATCH, VERTEX_PARALLEL, PlanForest,
                    SearchPlan, as_forest, emit_source, iter_nodes)
 
@@ -277,6 +278,25 @@ def _lgs_clique_k(g: Graph, forest: PlanForest, tasks, sink, index) -> int:
     return p.size if p.size in LGS_CLIQUE_K else 0
 
 
+def _is_cycle4_count(g: Graph, forest: PlanForest, tasks, sink, index) -> bool:
+    """A single count-only, unlabeled, edge-induced 4-cycle plan on a
+    symmetric graph over its implicit (whole or round-robin) task list: the
+    wedge-aggregation kernels (g2m_cycle4_count) give the same count."""
+    if len(forest.plans) != 1 or index is not None or g.labels is not None or g.oriented:
+        return False
+    pl = forest.single()
+    p = pl.pattern
+    if not (p.size == 4 and len(p.edges) == 4 and all(p.degree(v) == 2 for v in range(4))):
+        return False
+    if p.induced != EDGE_INDUCED or p.labels is not None or pl.uses_orientation:
+        return False
+    if sink is not None and pl.mode == "list":
+        return False
+    if isinstance(tasks, EdgeTaskList):
+        return tasks.is_implicit
+    return isinstance(tasks, VertexTasks)
+
+
 def _has_emitters(forest: PlanForest) -> bool:
     return any(a == EMIT_MATCH for r in forest.roots for n in iter_nodes(r)
                for a, _ in n.actions.values())
@@ -306,6 +326,18 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
                                          N.ptr(words, C.c_uint64), C.byref(stats)), "clique")
         pid = forest.pattern_ids[0]
         return {pid: int(words[0]) | (int(words[1]) << 64)}, stats, False, cp
+    if lgs and not instrument and _is_cycle4_count(g, forest, tasks, sink, index):
+        spec = N.TaskSpec()
+        spec.kind = N.TASKS_VERTEX
+        if rr is not None:
+            spec.rr_chunk, spec.rr_parts, spec.rr_part = rr
+        words = np.zeros(2, dtype=np.uint64)
+        stats = N.RunStats()
+        cfg = run_config if run_config is not None else N.RunConfig()
+        N.check(N.lib().g2m_cycle4_count(dg.handle, C.byref(spec), C.byref(cfg),
+                                         N.ptr(words, C.c_uint64), C.byref(stats)), "cycle4")
+        pid = forest.pattern_ids[0]
+        return {pid: int(words[0]) | (int(words[1]) << 64)}, stats, False, None
     list_mode = sink is not None and _has_emitters(forest)
     cp = compile_forest(forest, labeled, list_mode, dg.max_degree, flatten=flatten,
                         instrument=instrument)

@@ -390,3 +390,30 @@ def test_rmat12_lgs_known_counts():
         f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
         got, _, _, _ = EX.execute(og, f, EX._default_tasks(og, f), lgs=True)
         assert got[f.pattern_ids[0]] == want
+
+
+def test_cycle4_wedge_kernels_match_generic_and_oracle():
+    """g2m_cycle4_count (warp / CTA-hash / dense-HBM tiers) == the generated
+    4-cycle plan kernel == the oracle; K_n has 3*C(n,4) 4-cycles."""
+    graphs = [complete(4), complete(30), er(200, 0.1, 17), er(120, 0.3, 4),
+              GR.from_edges(G.rmat_edges(12, 16, 1), num_vertices=1 << 12),
+              GR.from_edges(G.rmat_edges(14, 16, 2), num_vertices=1 << 14),
+              GR.from_edges(G.powerlaw_edges(5000, 4, 3), num_vertices=5000)]
+    for g in graphs:
+        pl = make_plan(cycle4(), g)
+        f = PL.as_forest(pl)
+        tasks = EX._default_tasks(g, f)
+        a, _, _, _ = EX.execute(g, f, tasks, lgs=True)
+        b, _, _, _ = EX.execute(g, f, tasks, lgs=False)
+        assert a == b, g
+        if g.num_edges < 100000:
+            want, _ = O.run(g, f)
+            assert a == want
+    assert pm.subgraph_listing(complete(30), cycle4(), mode="count").counts["4-cycle"] == 3 * comb(30, 4)
+    g = GR.from_edges(G.rmat_edges(12, 16, 1), num_vertices=1 << 12)
+    assert pm.subgraph_listing(g, cycle4(), mode="count").counts["4-cycle"] == 52799071
+    # chunked round-robin shares of the top vertex add up to the whole
+    f = PL.as_forest(make_plan(cycle4(), g))
+    tasks = EX._default_tasks(g, f)
+    parts = [EX.execute(g, f, tasks, rr=(64, 3, i))[0]["4-cycle"] for i in range(3)]
+    assert sum(parts) == 52799071
