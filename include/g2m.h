@@ -34,6 +34,9 @@
  *   g2m_cycle4_count        run_dfs for the count-mode 4-cycle plan
  *                            (executor.py:339-408 over plan.py:110-174):
  *                            same count, wedge-aggregation kernels.
+ *   g2m_diamond_count       run_dfs for the count-mode diamond plan with
+ *                            the counting rewrite (executor.py:204-216):
+ *                            same count, edge triangle-support kernels.
  *   g2m_setop_batch         setops.intersect/intersect_count/difference/
  *                            difference_count (setops.py:35-84) as a
  *                            batched device call (kernel-library parity).
@@ -195,6 +198,15 @@ int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
  * share. counts_lo_hi receives (lo, hi). */
 int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, const g2m_run_config* cfg,
                      uint64_t* counts_lo_hi, g2m_run_stats* stats);
+
+/* Diamond count of a SYMMETRIC graph: the count-mode result of
+ * subgraph_listing(g, diamond) with the counting rewrite (apps.py:133-150,
+ * plan.py:177-198), Σ over edges of C(common neighbours, 2), from per-edge
+ * triangle support accumulated by the bitmap triangle kernels on the
+ * degree-oriented rank-space DAG. Single device (support is not additive
+ * over task partitions). counts_lo_hi receives (lo, hi). */
+int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, uint64_t* counts_lo_hi,
+                      g2m_run_stats* stats);
 
 /* Batched sorted-set kernels (setops.py:35-84). Lists are concatenated u32
  * arrays addressed by u64 offsets; op: 0 intersect, 1 intersect_count,

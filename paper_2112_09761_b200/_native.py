@@ -99,6 +99,7 @@ SIGNATURES = {
                                    _u64p, C.POINTER(RunStats)]),
     "g2m_cycle4_count": (C.c_int, [_P, C.POINTER(TaskSpec), C.POINTER(RunConfig), _u64p,
                                    C.POINTER(RunStats)]),
+    "g2m_diamond_count": (C.c_int, [_P, C.POINTER(RunConfig), _u64p, C.POINTER(RunStats)]),
     "g2m_setop_batch": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _u32p, _u64p, _u32p,
                                   _u64p, _i64p, _u64p, _u32p]),
 }

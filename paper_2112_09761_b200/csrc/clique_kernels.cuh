@@ -62,15 +62,26 @@ struct HashProbe {            // linear probing, load <= 1/2
     __device__ __forceinline__ bool has(u32 x) const { return get(x) != G2M_EMPTY; }
 };
 
+// Per-edge triangle support (diamond counting, k = 3 only): every triangle
+// u -> a -> x (u the source, a = A[i], x = A[pos]) adds 1 to the support of
+// its three DAG edges: (a, x) directly in t[] (other sources share it), and
+// (u, a), (u, x) through per-source shared row / column counters that are
+// flushed once per source.
+struct Support {
+    u32* t;       // t[slot] over the rank-space DAG slots
+    u32* row;     // shared, by local id
+    u32* col;
+};
+
 // Warp tier: probe the out-lists of rows [i0, i0+32) of A (scratch: 128
 // words: end[32] row[32] base[32 u64]). K == 3 returns the number of
 // members found (triangles u, A[i], x); otherwise sets the row bits of R
 // (row stride Ws words) and returns 0. All 32 lanes share the concatenated
 // lists (load-balanced whatever the list lengths).
-template <int K, typename Probe>
+template <int K, bool SUP = false, typename Probe>
 __device__ __forceinline__ u32 probe_rows(const u64* __restrict__ off, const u32* __restrict__ nbr,
                                           const u32* A, u32 d, u32 i0, u64* R, u32 Ws,
-                                          u32* scratch, const Probe& P) {
+                                          u32* scratch, const Probe& P, const Support& S = {}) {
     const u32 lane = g2m_lane();
     u32* fl_end = scratch;
     u32* fl_row = scratch + 32;
@@ -96,8 +107,16 @@ __device__ __forceinline__ u32 probe_rows(const u64* __restrict__ off, const u32
     u32 ow = 0;
     for (u32 e = lane; e < tot; e += 32) {
         while (fl_end[ow] <= e) ++ow;
-        const u32 x = __ldg(nbr + (fl_base[ow] + e));
-        if constexpr (K == 3) {
+        const u64 xi = fl_base[ow] + e;
+        const u32 x = __ldg(nbr + xi);
+        if constexpr (SUP) {
+            const u32 pos = P.get(x);
+            if (pos != G2M_EMPTY) {
+                atomicAdd(S.t + xi, 1u);
+                atomicAdd(S.row + fl_row[ow], 1u);
+                atomicAdd(S.col + pos, 1u);
+            }
+        } else if constexpr (K == 3) {
             hits += P.has(x) ? 1u : 0u;
         } else {
             const u32 pos = P.get(x);
@@ -131,11 +150,13 @@ struct Chain1<1> {
 // ---------------------------------------------------------------------------
 // warp tier: d <= 64, one warp per source vertex
 // ---------------------------------------------------------------------------
-template <int K, int WPB>
+template <int K, int WPB, bool SUP = false>
 __global__ void __launch_bounds__(WPB * 32)
 k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-              u64 nverts, u64* next, u64 grab, u64* count) {
+              u64 nverts, u64* next, u64 grab, u64* count, u32* tsup) {
     __shared__ u32 sA[WPB][64];
+    __shared__ u32 sRow[SUP ? WPB : 1][64];
+    __shared__ u32 sCol[SUP ? WPB : 1][64];
     __shared__ __align__(8) u64 sR[WPB][64];
     __shared__ __align__(8) u32 sScr[WPB][128];
     __shared__ u32 sHK[WPB][128];
@@ -165,9 +186,21 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
             const u32 hl = g2m_hlog(d);
             g2m_hmap_build(sHK[w], sHV[w], hl, A, d, lane, 32);
             const HashProbe P{sHK[w], sHV[w], hl, A[0], A[d - 1]};
-            u32 h = probe_rows<K>(off, nbr, A, d, 0, R, 1, sScr[w], P);
-            if (d > 32) h += probe_rows<K>(off, nbr, A, d, 32, R, 1, sScr[w], P);
-            if constexpr (K == 3) {
+            Support S{};
+            if constexpr (SUP) {
+                S = Support{tsup, sRow[w], sCol[w]};
+                sRow[w][lane] = sRow[w][lane + 32] = 0;
+                sCol[w][lane] = sCol[w][lane + 32] = 0;
+                __syncwarp();
+            }
+            u32 h = probe_rows<K, SUP>(off, nbr, A, d, 0, R, 1, sScr[w], P, S);
+            if (d > 32) h += probe_rows<K, SUP>(off, nbr, A, d, 32, R, 1, sScr[w], P, S);
+            if constexpr (SUP) {
+                for (u32 i = lane; i < d; i += 32) {
+                    const u32 c = sRow[w][i] + sCol[w][i];
+                    if (c) atomicAdd(tsup + b + i, c);
+                }
+            } else if constexpr (K == 3) {
                 acc += h;
             } else {
                 for (u32 i = lane; i < d; i += 32) acc += Chain1<K - 2>::run(R, R[i]);
@@ -207,8 +240,10 @@ __host__ __device__ constexpr size_t cta_row_words(int K, int W, int NW) {
 
 // Shared-memory bytes of one CTA-tier block (layout in k_clique_cta); with
 // GR the rows live in a global (L2-resident) slab per block instead.
-__host__ __device__ constexpr size_t cta_smem_bytes(int K, int W, int NW, u32 bmw, bool GR = false) {
+__host__ __device__ constexpr size_t cta_smem_bytes(int K, int W, int NW, u32 bmw, bool GR = false,
+                                                    bool SUP = false) {
     return (GR ? 0 : (size_t)8 * cta_row_words(K, W, NW))        // R, T
+           + (SUP ? (size_t)4 * 2 * 64 * W : 0)                  // support row / column counters
            + (size_t)8 * 64 * W                                  // RB
            + (size_t)4 * 64 * W * 2 + (size_t)4 * 2 * W          // A, RE, BT
            + (size_t)4 * 256 * W                                 // hash keys + vals
@@ -221,9 +256,9 @@ __host__ __device__ constexpr size_t cta_smem_bytes(int K, int W, int NW, u32 bm
 // same number of elements, whatever the row lengths). RE[i] is the
 // inclusive end of row i in the concatenation, RB[i] the nbr index of its
 // position 0. K == 3 counts members; otherwise sets the row bits of R.
-template <int K, int NW, typename Probe>
+template <int K, int NW, bool SUP, typename Probe>
 __device__ __forceinline__ u32 cta_probe(const u32* __restrict__ nbr, const u32* RE, const u64* RB, u32 d,
-                                         u32 tot, u32 w, u64* R, u32 Ws, const Probe& P) {
+                                         u32 tot, u32 w, u64* R, u32 Ws, const Probe& P, const Support& S) {
     const u32 lane = g2m_lane();
     u32 hits = 0;
     u32 o0 = 0;      // first row whose end is beyond the warp's first element (warp-uniform)
@@ -246,7 +281,24 @@ __device__ __forceinline__ u32 cta_probe(const u32* __restrict__ nbr, const u32*
             while (RE[ob] <= eb) ++ob;
             xb = __ldg(nbr + (RB[ob] + eb));
         }
-        if constexpr (K == 3) {
+        if constexpr (SUP) {
+            if (ea < tot) {
+                const u32 pos = P.get(xa);
+                if (pos != G2M_EMPTY) {
+                    atomicAdd(S.t + (RB[oa] + ea), 1u);
+                    atomicAdd(S.row + oa, 1u);
+                    atomicAdd(S.col + pos, 1u);
+                }
+            }
+            if (eb < tot) {
+                const u32 pos = P.get(xb);
+                if (pos != G2M_EMPTY) {
+                    atomicAdd(S.t + (RB[ob] + eb), 1u);
+                    atomicAdd(S.row + ob, 1u);
+                    atomicAdd(S.col + pos, 1u);
+                }
+            }
+        } else if constexpr (K == 3) {
             hits += (ea < tot && P.has(xa)) ? 1u : 0u;
             hits += (eb < tot && P.has(xb)) ? 1u : 0u;
         } else {
@@ -277,10 +329,10 @@ __device__ __forceinline__ u32 cta_probe(const u32* __restrict__ nbr, const u32*
 // compacted again and shared by the whole warp.
 // bmw: u32 words of the window bitmap (0 = hash only).
 // ---------------------------------------------------------------------------
-template <int K, int W, int NW, bool GR = false>
+template <int K, int W, int NW, bool GR = false, bool SUP = false>
 __global__ void __launch_bounds__(NW * 32)
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows) {
+             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows, u32* tsup) {
     constexpr u32 CH = 4;             // words compacted per round (<= 256 candidates)
     extern __shared__ __align__(16) u64 smem[];
     // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64   (K > 3 only)
@@ -297,6 +349,8 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
     u32* scr = HV + 128 * W;
     u32* BM = scr + NW * cta_warp_words(K);
     u16* PRE = (u16*)(BM + bmw);
+    u32* SROW = (u32*)(PRE + ((bmw + 1) & ~1u));     // SUP only: [64W] row, [64W] column counters
+    u32* SCOL = SROW + 64 * W;
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
     u32* L1 = scr + w * cta_warp_words(K);
@@ -350,6 +404,8 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         }
         if constexpr (K > 3)
             for (u32 x = threadIdx.x; x < d * Ws; x += NW * 32) R[x] = 0;
+        if constexpr (SUP)
+            for (u32 x = threadIdx.x; x < d; x += NW * 32) SROW[x] = SCOL[x] = 0;
         __syncthreads();
         u32 hl = 0;
         if (!use_bm) {
@@ -385,12 +441,18 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         // ---- build rows (K > 3) / count triangles (K == 3)
         const u32 tot = s_tot;
         u32 hits;
+        const Support S{tsup, SROW, SCOL};
         if (use_bm)
-            hits = cta_probe<K, NW>(nbr, RE, RB, d, tot, w, R, Ws, BitmapProbe{BM, PRE, a0, span});
+            hits = cta_probe<K, NW, SUP>(nbr, RE, RB, d, tot, w, R, Ws, BitmapProbe{BM, PRE, a0, span}, S);
         else
-            hits = cta_probe<K, NW>(nbr, RE, RB, d, tot, w, R, Ws, HashProbe{HK, HV, hl, a0, alast});
+            hits = cta_probe<K, NW, SUP>(nbr, RE, RB, d, tot, w, R, Ws, HashProbe{HK, HV, hl, a0, alast}, S);
         if constexpr (K == 3) acc += hits;
         __syncthreads();
+        if constexpr (SUP)
+            for (u32 x = threadIdx.x; x < d; x += NW * 32) {
+                const u32 c = SROW[x] + SCOL[x];
+                if (c) atomicAdd(tsup + b + x, c);
+            }
         if constexpr (K > 3) {
             for (;;) {
                 u32 i = 0;
@@ -538,6 +600,18 @@ __global__ void k_clique_bucket(const u64* off, const u32* nbr, u64 nv, int kmin
         lists[(u64)c * list_stride + slot] = (u32)v;
         if (c >= 2 && c != 6) atomicMax(span_max + c, __ldg(nbr + b + d - 1) - __ldg(nbr + b) + 1u);
     }
+}
+
+// Σ_e C(t_e, 2): diamonds from per-edge triangle support (diamond = an edge
+// plus an unordered pair of its common neighbours).
+__global__ void k_sum_choose2(const u32* t, u64 n, u64* count) {
+    u64 acc = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 c = t[i];
+        acc += c * (c - 1) / 2;
+    }
+    acc = g2m_wsum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) g2m_add128(count, acc, 0);
 }
 
 }  // namespace g2m_clique

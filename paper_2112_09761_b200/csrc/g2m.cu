@@ -193,6 +193,8 @@ struct g2m_graph {
     // the same graph relabelled by its (degree, id) order, lazily built
     DevBuf rk_off, rk_nbr;
     bool has_rank = false;
+    // symmetric graphs: degree orientation, lazily built (diamond support)
+    std::unique_ptr<g2m_graph> oriented_copy;
 };
 
 __global__ void k_max_degree(const u64* off, u64 nv, u64* out) {
@@ -357,13 +359,7 @@ static int exclusive_scan_u64(DevState* st, const u64* in, u64* out, uint64_t n)
     return G2M_OK;
 }
 
-extern "C" int g2m_graph_orient(const g2m_graph* g, g2m_graph** out) {
-    if (!g || !out) return fail(G2M_EUSAGE, "null argument");
-    if (g->oriented) return fail(G2M_EUSAGE, "graph is already oriented");
-    DevState* st;
-    G2M_TRY(dev_state(g->dev, &st));
-    std::lock_guard<std::mutex> lk(st->mu);
-    G2M_CUDA(cudaSetDevice(g->dev));
+static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     auto o = std::make_unique<g2m_graph>();
     o->dev = g->dev;
     o->nv = g->nv;
@@ -393,6 +389,16 @@ extern "C" int g2m_graph_orient(const g2m_graph* g, g2m_graph** out) {
     G2M_TRY(finish_graph(o.get(), st));
     *out = o.release();
     return G2M_OK;
+}
+
+extern "C" int g2m_graph_orient(const g2m_graph* g, g2m_graph** out) {
+    if (!g || !out) return fail(G2M_EUSAGE, "null argument");
+    if (g->oriented) return fail(G2M_EUSAGE, "graph is already oriented");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    return orient_impl(g, st, out);
 }
 
 extern "C" int g2m_graph_replicate(const g2m_graph* g, int32_t device, g2m_graph** out) {
@@ -1100,9 +1106,10 @@ __global__ void k_heavy_fill(const u64* off, const u32* verts, u64 n, const u64*
 // 7 CTA tier W = 64 (k = 3 only: no rows), 6 generic plan kernel.
 static const int kClasses = 8;
 
-template <int K>
+template <int K, bool SUP = false>
 static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const u32* lists, u64 stride,
-                             const uint64_t* sizes, const uint32_t* spans, u64* ctr, double* kms) {
+                             const uint64_t* sizes, const uint32_t* spans, u64* ctr, double* kms,
+                             u32* tsup = nullptr) {
     using namespace g2m_clique;
     u64* count = ctr;        // (lo, hi)
     u64* next = ctr + 2;     // one work counter per launch
@@ -1125,8 +1132,8 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         u64 grab = std::max<u64>(1, std::min<u64>(8, sizes[1] / ((u64)st->sms * 64 * WPB)));
         G2M_TRY(timed([&] {
             ++st->launches;
-            k_clique_warp<K, WPB><<<st->sms * 8, WPB * 32, 0, st->stream>>>(off, nbr, lists + 1 * stride,
-                                                                            sizes[1], next + slot, grab, count);
+            k_clique_warp<K, WPB, SUP><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
+                off, nbr, lists + 1 * stride, sizes[1], next + slot, grab, count, tsup);
         }));
         ++slot;
     }
@@ -1142,13 +1149,13 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         if (!sizes[cls]) return G2M_OK;
         // window bitmap: as wide as the widest source of the class needs, within
         // the shared memory left at `want_ctas` blocks per SM
-        const size_t base = cta_smem_bytes(K, W, NW, 0, GR);
+        const size_t base = cta_smem_bytes(K, W, NW, 0, GR, SUP);
         const size_t per_block = std::min<size_t>((size_t)max_smem, (size_t)sm_smem / want_ctas - 1024);
         u32 bmw = 0;
         if (per_block > base + 64) bmw = (u32)std::min<size_t>((per_block - base) / 6, ((size_t)spans[cls] + 31) / 32);
         bmw &= ~1u;
-        const size_t smem = cta_smem_bytes(K, W, NW, bmw, GR);
-        auto kern = k_clique_cta<K, W, NW, GR>;
+        const size_t smem = cta_smem_bytes(K, W, NW, bmw, GR, SUP);
+        auto kern = k_clique_cta<K, W, NW, GR, SUP>;
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
         G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
@@ -1164,7 +1171,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         G2M_TRY(timed([&] {
             ++st->launches;
             kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
-                                                                 next + slot, count, bmw, grows);
+                                                                 next + slot, count, bmw, grows, tsup);
         }));
         ++slot;
         return G2M_OK;
@@ -1294,6 +1301,97 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     counts[1] = (uint64_t)(total >> 64);
     G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
     G2M_CUDA(cudaEventSynchronize(st->evs1));
+    float dm = 0.f;
+    cudaEventElapsedTime(&dm, st->evs0, st->evs1);
+    S->device_ms = dm;
+    S->launches = st->launches - l0;
+    S->total_ms = ms_since(t0);
+    return G2M_OK;
+}
+
+// ---------------------------------------------------------------------------
+// diamond count from per-edge triangle support
+// ---------------------------------------------------------------------------
+// Edge-induced diamonds = Σ over edges {u, v} of C(|N(u) ∩ N(v)|, 2): the
+// count the reference's counting rewrite evaluates per edge task
+// (plan.py:177-198, executor.py:204-216). |N(u) ∩ N(v)| is the number of
+// triangles on the edge, accumulated by the bitmap triangle kernels over the
+// rank-space DAG of the degree orientation (one support counter per DAG edge).
+
+extern "C" int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, uint64_t* counts,
+                                 g2m_run_stats* stats) {
+    (void)cfg;
+    if (!g || !counts) return fail(G2M_EUSAGE, "null argument");
+    if (g->oriented) return fail(G2M_EUSAGE, "plan orientation does not match the graph");
+    auto t0 = Clock::now();
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    g2m_run_stats local{};
+    g2m_run_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    const uint64_t l0 = st->launches;
+    g2m_graph* gm = const_cast<g2m_graph*>(g);
+    {
+        std::lock_guard<std::mutex> glk(gm->mu);
+        if (!gm->oriented_copy) {
+            g2m_graph* o = nullptr;
+            G2M_TRY(orient_impl(g, st, &o));
+            gm->oriented_copy.reset(o);
+        }
+    }
+    const g2m_graph* og = gm->oriented_copy.get();
+    G2M_TRY(ensure_rank(og, st));
+    const u64* off = og->rk_off.as<u64>();
+    const u32* nbr = og->rk_nbr.as<u32>();
+    G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
+    G2M_TRY(st->counters.ensure(32 * 8));
+    u64* ctr = st->counters.as<u64>();
+    G2M_CUDA(cudaMemsetAsync(ctr, 0, 32 * 8, st->stream));
+    DevBuf tsup;
+    G2M_TRY(tsup.ensure(std::max<u64>(og->slots, 1) * 4));
+    G2M_CUDA(cudaMemsetAsync(tsup.p, 0, std::max<u64>(og->slots, 1) * 4, st->stream));
+    const u64 stride = std::max<u64>(og->nv, 1);
+    G2M_TRY(st->tasks_b.ensure((u64)kClasses * stride * 4));
+    G2M_TRY(st->tasks_a.ensure(kClasses * 8 + kClasses * 4));
+    u64* dsizes = st->tasks_a.as<u64>();
+    u32* dspans = (u32*)(dsizes + kClasses);
+    G2M_CUDA(cudaMemsetAsync(dsizes, 0, kClasses * 12, st->stream));
+    if (og->nv) {
+        ++st->launches;
+        g2m_clique::k_clique_bucket<<<grid_for(st, og->nv, 256), 256, 0, st->stream>>>(
+            off, nbr, og->nv, 2, 4096, 0, 1, 0, st->tasks_b.as<u32>(), stride, dsizes, dspans);
+        G2M_CUDA(cudaGetLastError());
+    }
+    uint64_t sizes[kClasses];
+    uint32_t spans[kClasses];
+    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, kClasses * 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaMemcpyAsync(spans, dspans, kClasses * 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    if (sizes[6]) return fail(G2M_EUSAGE, "diamond support kernels cover out-degrees <= 4096");
+    G2M_TRY((clique_launch_all<3, true>(off, nbr, st, st->tasks_b.as<u32>(), stride, sizes, spans, ctr + 8,
+                                         &S->kernel_ms, tsup.as<u32>())));
+    {
+        G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
+        ++st->launches;
+        g2m_clique::k_sum_choose2<<<grid_for(st, og->slots, 256), 256, 0, st->stream>>>(tsup.as<u32>(), og->slots,
+                                                                                           ctr + 16);
+        G2M_CUDA(cudaGetLastError());
+        G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
+        G2M_CUDA(cudaEventSynchronize(st->ev1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, st->ev0, st->ev1);
+        S->kernel_ms += ms;
+    }
+    uint64_t h[2] = {0, 0};
+    G2M_CUDA(cudaMemcpyAsync(h, ctr + 16, 16, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
+    G2M_CUDA(cudaEventSynchronize(st->evs1));
+    counts[0] = h[0];
+    counts[1] = h[1];
+    S->tasks = 0;
+    for (int c = 1; c < kClasses; ++c) S->tasks += sizes[c];
     float dm = 0.f;
     cudaEventElapsedTime(&dm, st->evs0, st->evs1);
     S->device_ms = dm;

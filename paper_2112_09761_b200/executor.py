@@ -297,6 +297,28 @@ def _is_cycle4_count(g: Graph, forest: PlanForest, tasks, sink, index) -> bool:
     return isinstance(tasks, VertexTasks)
 
 
+def _is_diamond_count(g: Graph, forest: PlanForest, tasks, sink, index, rr) -> bool:
+    """A single count-only, unlabeled, edge-induced diamond plan on a
+    symmetric graph over its whole implicit task list (one device): the
+    edge triangle-support kernels (g2m_diamond_count) give the same count."""
+    if len(forest.plans) != 1 or index is not None or rr is not None:
+        return False
+    if g.labels is not None or g.oriented:
+        return False
+    pl = forest.single()
+    p = pl.pattern
+    if not (p.size == 4 and len(p.edges) == 5
+            and sorted(p.degree(v) for v in range(4)) == [2, 2, 3, 3]):
+        return False
+    if p.induced != EDGE_INDUCED or p.labels is not None or pl.uses_orientation:
+        return False
+    if sink is not None and pl.mode == "list":
+        return False
+    if isinstance(tasks, EdgeTaskList):
+        return tasks.is_implicit
+    return isinstance(tasks, VertexTasks)
+
+
 def _has_emitters(forest: PlanForest) -> bool:
     return any(a == EMIT_MATCH for r in forest.roots for n in iter_nodes(r)
                for a, _ in n.actions.values())
@@ -338,6 +360,17 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
                                          N.ptr(words, C.c_uint64), C.byref(stats)), "cycle4")
         pid = forest.pattern_ids[0]
         return {pid: int(words[0]) | (int(words[1]) << 64)}, stats, False, None
+    if lgs and not instrument and _is_diamond_count(g, forest, tasks, sink, index, rr):
+        words = np.zeros(2, dtype=np.uint64)
+        stats = N.RunStats()
+        cfg = run_config if run_config is not None else N.RunConfig()
+        rc = N.lib().g2m_diamond_count(dg.handle, C.byref(cfg), N.ptr(words, C.c_uint64),
+                                       C.byref(stats))
+        if rc == N.G2M_OK:
+            pid = forest.pattern_ids[0]
+            return {pid: int(words[0]) | (int(words[1]) << 64)}, stats, False, None
+        if rc != N.G2M_EUSAGE:          # out-degree beyond the tiers: generated kernel below
+            N.check(rc, "diamond")
     list_mode = sink is not None and _has_emitters(forest)
     cp = compile_forest(forest, labeled, list_mode, dg.max_degree, flatten=flatten,
                         instrument=instrument)

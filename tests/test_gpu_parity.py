@@ -417,3 +417,26 @@ def test_cycle4_wedge_kernels_match_generic_and_oracle():
     tasks = EX._default_tasks(g, f)
     parts = [EX.execute(g, f, tasks, rr=(64, 3, i))[0]["4-cycle"] for i in range(3)]
     assert sum(parts) == 52799071
+
+
+def test_diamond_support_kernels_match_generic_and_oracle():
+    """g2m_diamond_count (edge triangle support over the rank-space DAG) ==
+    the generated diamond plan kernel (counting rewrite) == the oracle."""
+    graphs = [complete(4), complete(40), er(200, 0.1, 17), er(120, 0.3, 4),
+              GR.from_edges(G.rmat_edges(12, 16, 1), num_vertices=1 << 12),
+              GR.from_edges(G.rmat_edges(14, 16, 2), num_vertices=1 << 14),
+              GR.from_edges(G.powerlaw_edges(5000, 4, 3), num_vertices=5000),
+              _heavy_source_graph()]
+    for g in graphs:
+        pl = make_plan(diamond(), g, rewrite=True)
+        f = PL.as_forest(pl)
+        tasks = EX._default_tasks(g, f)
+        a, _, _, _ = EX.execute(g, f, tasks, lgs=True)
+        b, _, _, _ = EX.execute(g, f, tasks, lgs=False)
+        assert a == b, g
+        if g.num_edges < 100000:
+            want, _ = O.run(g, f)
+            assert a == want
+    assert pm.subgraph_listing(complete(40), diamond(), mode="count").counts["diamond"] == 6 * comb(40, 4)
+    g = GR.from_edges(G.rmat_edges(12, 16, 1), num_vertices=1 << 12)
+    assert pm.subgraph_listing(g, diamond(), mode="count").counts["diamond"] == 57343012
