@@ -266,6 +266,7 @@ def main():
               "graph": f"{spec[0]}{spec[1]}", "num_vertices": g.num_vertices,
               "undirected_edges": E, "oriented": gd.oriented, "max_degree_task_graph": gd.max_degree,
               "granularity": pj.granularity, "tasks": len(tasks),
+              "search": next((d.render() for d in pj.log if d.name == "bounded-bfs"), "dfs"),
               "parallelism": f"{world} GPU(s), chunked round-robin tasks, graph replicated"
               if world > 1 else "1 GPU",
               "l2": "inputs larger than L2 (CSR > 126 MB); no flush needed" if gd.num_edges * 4 > 126e6
@@ -297,8 +298,8 @@ def main():
     # ------------------------------------------------------------------ b200
     rr = (256, world, rank) if world > 1 else None
 
-    def step():
-        counts, st, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr)
+    def step():   # run_job's search choice (DFS / bounded-frontier BFS), logged as "bounded-bfs"
+        counts, st, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, search="auto")
         return counts, st
 
     for _ in range(args.warmup):
@@ -350,7 +351,7 @@ def main():
                 api_call(args.workload, hg)
             else:
                 pr = prepare(args.workload, hg)
-                EX.execute(pr.graph, pr.forest, pr.tasks, device=local, rr=rr)
+                EX.execute(pr.graph, pr.forest, pr.tasks, device=local, rr=rr, search="auto")
             dt = time.perf_counter() - t1
             del hg
             if i >= nw:

@@ -27,6 +27,9 @@
  *                            run_dfs_lgs executor.py:526-599; one call per
  *                            device -- scheduler.run_on_devices
  *                            (scheduler.py:207-239) issues one per GPU.
+ *   g2m_run_bfs             run_dfs through the bounded-frontier BFS
+ *                            runtime (same counts; DFS/BFS chooser in
+ *                            executor.choose_search).
  *   g2m_list                run_dfs(..., sink) list mode: matches are
  *                            produced on the device in exact reference
  *                            order (task order, then DFS order) and handed
@@ -178,6 +181,20 @@ int g2m_run(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* tasks,
 int g2m_list(const g2m_kernel* k, const g2m_graph* g, const g2m_task_spec* tasks,
              const g2m_run_config* cfg, g2m_match_cb cb, void* user,
              uint64_t* counts_lo_hi, g2m_run_stats* stats);
+
+/* Bounded-frontier BFS runtime (run_dfs semantics, executor.py:339-408;
+ * the level-synchronous extension of PAPER.md Alg. 2 / test_executor.py:
+ * 203-235 restricted to the first three levels). `expand` and `consume` are
+ * the two frontier kernels of one edge-parallel count forest (codegen
+ * frontier="expand"/"consume"). Tasks are processed in blocks; each block's
+ * level-3 candidates become work items of `chunk` candidates that the
+ * consume kernel finishes depth-first, so hub edges are split across warps.
+ * The item buffer is at most `frontier_bytes` (0: a quarter of free HBM);
+ * a block that overflows it is halved and redone. stats->high_water[6] =
+ * blocks, [7] = peak items. Counts equal g2m_run's. */
+int g2m_run_bfs(const g2m_kernel* expand, const g2m_kernel* consume, const g2m_graph* g,
+                const g2m_task_spec* tasks, const g2m_run_config* cfg, uint32_t chunk,
+                uint64_t frontier_bytes, uint64_t* counts_lo_hi, g2m_run_stats* stats);
 
 /* k-clique count (3 <= k <= 5) on an ORIENTED graph with the bitmap
  * local-graph kernels (one local DAG per source vertex; setops.py:101-173,

@@ -95,6 +95,8 @@ SIGNATURES = {
                           C.POINTER(RunStats)]),
     "g2m_list": (C.c_int, [_P, _P, C.POINTER(TaskSpec), C.POINTER(RunConfig), MATCH_CB,
                            C.c_void_p, _u64p, C.POINTER(RunStats)]),
+    "g2m_run_bfs": (C.c_int, [_P, _P, _P, C.POINTER(TaskSpec), C.POINTER(RunConfig), C.c_uint32,
+                              C.c_uint64, _u64p, C.POINTER(RunStats)]),
     "g2m_clique_count": (C.c_int, [_P, C.c_int32, C.POINTER(TaskSpec), _P, C.POINTER(RunConfig),
                                    _u64p, C.POINTER(RunStats)]),
     "g2m_cycle4_count": (C.c_int, [_P, C.POINTER(TaskSpec), C.POINTER(RunConfig), _u64p,

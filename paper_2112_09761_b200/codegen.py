@@ -91,8 +91,10 @@ def _is_count(action: str) -> bool:
 class _Gen:
     def __init__(self, forest: PlanForest, labeled: bool, list_mode: bool,
                  smem_slot_cap: int, warps_per_block: int, stage_words: int,
-                 flatten: bool, instrument: bool = False):
+                 flatten: bool, instrument: bool = False, frontier: str | None = None):
         self.f = forest
+        self.frontier = frontier         # None | "expand" | "consume"
+        self.l3_ids: dict[int, int] = {}  # id(level-3 iterating node) -> item node id
         self.instrument = instrument
         self.labeled = labeled
         self.list_mode = list_mode
@@ -124,6 +126,14 @@ class _Gen:
         self.hw_levels = 0
         self.stage_used = False
         self.fl_used = False
+        if frontier is not None:
+            if not self.edge or list_mode or instrument or labeled:
+                raise ValueError("frontier kernels need an unlabeled edge-parallel count forest")
+            for root in forest.roots:
+                for c in root.children:
+                    for gc in c.children:
+                        if _iterates(gc, False):
+                            self.l3_ids[id(gc)] = len(self.l3_ids)
 
     # -- helpers ------------------------------------------------------------
 
@@ -418,8 +428,11 @@ class _Gen:
             if buf_depth < 8:
                 o(f"hw{buf_depth} = max(hw{buf_depth}, s{L}n);")
             child_buf = buf_depth + 1
-        # ---- terminals applied at this node from the set (_count_from_set)
+        # ---- terminals applied at this node from the set (_count_from_set);
+        # a consume pass already had them applied by its expand pass
         cpids = [p for p in sorted(node.actions) if _is_count(node.actions[p][0])]
+        if self.frontier == "consume" and L == 3:
+            cpids = []
         for b, group in self.bound_groups(node, cpids).items():
             gm = self.mask_of(group)
             o.push(f"if ({mask} & {gm}u) {{")
@@ -465,6 +478,26 @@ class _Gen:
                     parts.append(f"(({idx_var}) < {cn} ? {gm}u : 0u)")
             return f"({mask} & ({' | '.join(parts)}))"
 
+        if self.frontier == "expand" and L == 3:
+            # bounded-frontier BFS: the level-3 candidates become work items
+            # of `fchunk` candidates each, (v1, v2, node, first index)
+            nid = self.l3_ids[id(node)]
+            o.push("if (maxcut) {")
+            o("const u32 nit = (maxcut + a.fchunk - 1u) / a.fchunk;")
+            o("u64 fb = 0;")
+            o("if (lane == 0) fb = atomicAdd(a.frontier_n, (u64)nit);")
+            o("fb = __shfl_sync(G2M_FULL, fb, 0);")
+            o.push("for (u32 q = lane; q < nit; q += 32) {")
+            o(f"if (fb + q < a.frontier_cap) a.frontier[fb + q] = G2MItem{{v1, v2, {nid}u, q * a.fchunk}};")
+            o.pop()
+            o.pop()
+            o.pop()
+            o.pop()
+            return
+        lo, hi = "0u", "maxcut"
+        if self.frontier == "consume" and L == 3:
+            o("const u32 flo = min(item.lo, maxcut), fhi = min(item.lo + a.fchunk, maxcut);")
+            lo, hi = "flo", "fhi"
         flat, loop_children = [], []
         for c in node.children:
             if self.flatten and self.flattenable(c, L):
@@ -474,10 +507,14 @@ class _Gen:
         for c in flat:
             cm = self.mask_of(c.members)
             o.push(f"if ({mask} & {cm}u) {{")
-            self.emit_flat(c, L, f"s{L}p", "maxcut", f"{mask_at('ci')} & {cm}u")
+            if lo == "0u":
+                self.emit_flat(c, L, f"s{L}p", "maxcut", f"{mask_at('ci')} & {cm}u")
+            else:
+                self.emit_flat(c, L, f"(s{L}p + {lo})", f"({hi} - {lo})",
+                               f"{mask_at(f'(ci + {lo})')} & {cm}u")
             o.pop()
         if loop_children or emitters:
-            o.push("for (u32 idx = 0; idx < maxcut; ++idx) {")
+            o.push(f"for (u32 idx = {lo}; idx < {hi}; ++idx) {{")
             o(f"const u32 cand = s{L}p[idx];")
             skip = " || ".join(f"cand == v{l}" for l in range(1, L))
             o(f"if ({skip}) continue;")
@@ -585,6 +622,32 @@ class _Gen:
             o.pop()
         o.pop()
 
+    def emit_consume_item(self) -> None:
+        """Consume pass of the bounded-frontier BFS: one item = (v1, v2,
+        level-3 node, first candidate index); re-evaluate that node's set and
+        run its subtree for candidates [lo, lo + fchunk)."""
+        o = self.o
+        o("const u32 cx = item.v2;")
+        o.push("switch (item.node) {")
+        for root in self.f.roots:
+            for c in root.children:
+                members = self.mask_of(c.members)
+                unbounded = self.mask_of([p for p in c.members if c.bounds[p] is None])
+                for gc in c.children:
+                    if id(gc) not in self.l3_ids:
+                        continue
+                    o.push(f"case {self.l3_ids[id(gc)]}u: {{")
+                    o(f"const u32 m2 = (u32)({unbounded}u | (cx < v1 ? {members}u : 0u));")
+                    self.bind_level(2, "cx")
+                    cm = self.mask_of(gc.members)
+                    o.push(f"if (m2 & {cm}u) {{")
+                    o(f"const u32 m2c = m2 & {cm}u;")
+                    self.emit_node(gc, "m2c", 0, 0)
+                    o.pop()
+                    o("break;")
+                    o.pop()
+        o.pop()
+
     def emit_vertex_task(self) -> None:
         """run_vertex_task (executor.py:284-295)."""
         o = self.o
@@ -610,7 +673,9 @@ class _Gen:
         o = self.o
         body_mark = len(o.lines)
         o.ind = 4
-        if self.edge:
+        if self.frontier == "consume":
+            self.emit_consume_item()
+        elif self.edge:
             self.emit_edge_group()
         else:
             self.emit_vertex_task()
@@ -670,7 +735,12 @@ class _Gen:
         w("        const u64 t1 = min(t0 + a.grab, a.ntasks);")
         w("        have_hint = false;")
         w("        for (u64 t = t0; t < t1;) {")
-        if self.edge:
+        if self.frontier == "consume":
+            w("            const G2MItem item = a.frontier[t];")
+            w("            t += 1;")
+            w("            {")
+            w("                " + self._bind1_text().replace("v1_", "item.v1"))
+        elif self.edge:
             w("            u32 v1_; const u32* v2s; u32 n2; const u64 tgrp = t;")
             w("            if (a.source == 1) {")
             w("                v1_ = __ldg(a.t_src + t); v2s = a.t_dst + t;")
@@ -740,6 +810,19 @@ class _Gen:
         return "const u32 v1 = v1_;"
 
 
+def _iterates(node: PlanNode, list_mode: bool) -> bool:
+    return bool(node.children) or (list_mode and any(a == EMIT_MATCH for a, _ in node.actions.values()))
+
+
+def frontier_nodes(forest: PlanForest) -> int:
+    """Level-3 iterating nodes of an edge-parallel forest: the node ids of
+    the bounded-frontier BFS items (0 = nothing to split, DFS only)."""
+    if forest.parallel_granularity != EDGE_PARALLEL:
+        return 0
+    return sum(1 for root in forest.roots for c in root.children for gc in c.children
+               if _iterates(gc, False))
+
+
 def _as_counting(forest: PlanForest) -> PlanForest:
     """Count-only view of a forest: an EMIT_MATCH terminal without a sink
     just counts its candidates (executor.py:275-280 with sink=None), which is
@@ -785,9 +868,13 @@ def slots_needed(forest: PlanForest, labeled: bool) -> int:
 
 def generate(forest: PlanForest, *, labeled: bool = False, list_mode: bool = False,
              smem_slot_cap: int = 0, warps_per_block: int = 8, stage_words: int = 1024,
-             flatten: bool = True, instrument: bool = False) -> GeneratedKernel:
+             flatten: bool = True, instrument: bool = False,
+             frontier: str | None = None) -> GeneratedKernel:
     """Emit the CUDA source of one plan forest. ``smem_slot_cap`` > 0 keeps
     materialised sets in shared memory (capacity in u32 per slot); 0 puts
-    them in per-warp global scratch."""
+    them in per-warp global scratch. ``frontier`` = "expand" / "consume"
+    emits the two passes of the bounded-frontier BFS runtime: expand runs
+    levels 1-3 (terminals included) and writes the level-3 candidates as
+    work items; consume runs levels >= 4 for one item per task."""
     return _Gen(forest, labeled, list_mode, smem_slot_cap, warps_per_block,
-                stage_words, flatten, instrument).generate()
+                stage_words, flatten, instrument, frontier).generate()

@@ -984,6 +984,105 @@ extern "C" int g2m_run(const g2m_kernel* k, const g2m_graph* g, const g2m_task_s
     return G2M_OK;
 }
 
+// Bounded-frontier BFS: per block of tasks, the expand kernel runs levels
+// 1-3 (their terminals included) and writes the level-3 candidates as work
+// items of `chunk` candidates; the consume kernel runs levels >= 4 over the
+// items. A block whose frontier overflows the buffer is halved and redone
+// (its partial counts are discarded), so the frontier is bounded by
+// `frontier_bytes` whatever the graph.
+extern "C" int g2m_run_bfs(const g2m_kernel* ke, const g2m_kernel* kc, const g2m_graph* g,
+                           const g2m_task_spec* ts, const g2m_run_config* cfg, uint32_t chunk,
+                           uint64_t frontier_bytes, uint64_t* counts, g2m_run_stats* stats) {
+    if (!ke || !kc || !g || !ts) return fail(G2M_EUSAGE, "null argument");
+    if (ke->meta.num_patterns != kc->meta.num_patterns) return fail(G2M_EUSAGE, "expand/consume kernels differ");
+    if (chunk == 0) return fail(G2M_EUSAGE, "frontier chunk must be positive");
+    auto t0 = Clock::now();
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    g2m_run_stats local{};
+    g2m_run_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    const uint64_t l0 = st->launches;
+    Prepared P;
+    G2M_TRY(prepare_tasks(ke, g, ts, st, &P));
+    const uint64_t nt = P.a.ntasks;
+    S->tasks = nt;
+    const int np = std::max(ke->meta.num_patterns, 1);
+    std::vector<unsigned __int128> tot(np, 0);
+    size_t fr = 0, tb = 0;
+    cudaMemGetInfo(&fr, &tb);
+    uint64_t fbytes = frontier_bytes ? frontier_bytes : (uint64_t)fr / 4;
+    fbytes = std::min<uint64_t>(fbytes, (uint64_t)fr / 2);
+    const uint64_t cap = std::max<uint64_t>(fbytes / sizeof(G2MItem), 64);
+    DevBuf items, fn;
+    G2M_TRY(items.ensure(cap * sizeof(G2MItem)));
+    G2M_TRY(fn.ensure(8));
+    G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
+    uint64_t lo = 0, block = nt, peak = 0, blocks = 0;
+    std::vector<uint64_t> h(2 * np);
+    while (lo < nt) {
+        const uint64_t hi = std::min(nt, lo + block);
+        // expand levels 1-3 of tasks [lo, hi)
+        G2M_TRY(reset_counters(ke, st));
+        G2M_CUDA(cudaMemsetAsync(fn.p, 0, 8, st->stream));
+        G2MArgs a = P.a;
+        a.frontier = items.as<G2MItem>();
+        a.frontier_cap = cap;
+        a.frontier_n = fn.as<u64>();
+        a.fchunk = chunk;
+        G2M_TRY(launch(ke, g, st, a, cfg, lo, hi, &S->kernel_ms, &S->warps));
+        uint64_t nitems = 0;
+        G2M_CUDA(cudaMemcpyAsync(&nitems, fn.p, 8, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        if (nitems > cap) {   // frontier overflow: redo a smaller block
+            if (hi - lo == 1) return fail(G2M_EBUDGET, "one task's level-3 frontier exceeds the frontier buffer");
+            block = std::max<uint64_t>(1, (hi - lo) / 2);
+            continue;
+        }
+        G2M_TRY(collect(ke, st, h.data(), nullptr));
+        for (int p = 0; p < ke->meta.num_patterns; ++p)
+            tot[p] += ((unsigned __int128)h[2 * p + 1] << 64) | h[2 * p];
+        peak = std::max(peak, nitems);
+        ++blocks;
+        // consume levels >= 4 of the block's items
+        if (nitems) {
+            G2M_TRY(reset_counters(kc, st));
+            G2MArgs b;
+            std::memset(&b, 0, sizeof(b));
+            b.off = g->off.as<u64>();
+            b.nbr = g->nbr.as<u32>();
+            b.labels = g->labels.as<u32>();
+            b.nv = g->nv;
+            b.kind = G2M_TASKS_EDGE;
+            b.frontier = items.as<G2MItem>();
+            b.frontier_cap = cap;
+            b.fchunk = chunk;
+            G2M_TRY(launch(kc, g, st, b, cfg, 0, nitems, &S->kernel_ms, nullptr));
+            G2M_TRY(collect(kc, st, h.data(), nullptr));
+            for (int p = 0; p < kc->meta.num_patterns; ++p)
+                tot[p] += ((unsigned __int128)h[2 * p + 1] << 64) | h[2 * p];
+        }
+        lo = hi;
+    }
+    for (int p = 0; p < ke->meta.num_patterns; ++p) {
+        counts[2 * p] = (uint64_t)tot[p];
+        counts[2 * p + 1] = (uint64_t)(tot[p] >> 64);
+    }
+    G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
+    G2M_CUDA(cudaEventSynchronize(st->evs1));
+    float dm = 0.f;
+    cudaEventElapsedTime(&dm, st->evs0, st->evs1);
+    S->device_ms = dm;
+    S->high_water[6] = blocks;
+    S->high_water[7] = peak;
+    S->h2d_bytes += P.h2d;
+    S->launches = st->launches - l0;
+    S->total_ms = ms_since(t0);
+    return G2M_OK;
+}
+
 // List mode: a counting pass sizes every task's match stream, then batches
 // of whole tasks are re-run writing tuples at exact offsets, so the host sees
 // matches in reference order (task order, then DFS order).

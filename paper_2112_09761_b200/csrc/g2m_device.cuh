@@ -22,6 +22,12 @@ typedef long long i64;
 
 #define G2M_FULL 0xffffffffu
 
+// Bounded-frontier BFS work item: level-3 candidates [lo, lo + fchunk) of
+// level-3 node `node` under the edge task (v1, v2).
+struct G2MItem {
+    u32 v1, v2, node, lo;
+};
+
 // Layout shared with the host (g2m.cu). Plain old data only.
 struct G2MArgs {
     const u64* off;         // CSR row offsets [nv+1]
@@ -54,6 +60,12 @@ struct G2MArgs {
     u64 task_end;           // one past the last local task of this batch
     int list_pass;          // 0 count pass, 1 write pass
     int reserved;
+    // --- bounded-frontier BFS (level-3 frontier items: v1, v2, node, lo) ---
+    G2MItem* frontier;      // expand: item output; consume: item input
+    u64 frontier_cap;       // items that fit (expand)
+    u64* frontier_n;        // items produced (expand, may exceed cap)
+    u32 fchunk;             // level-3 candidates per item
+    u32 reserved2;
 };
 
 __device__ __forceinline__ u32 g2m_lane() { return threadIdx.x & 31u; }

@@ -47,6 +47,9 @@ class ExecutionConfig:
     lgs: str = "auto"                    # local graph search: auto | on | off
     lgs_delta_threshold: int = 1024
     bfs_block_size: int = 1 << 20
+    search: str = "auto"                 # dfs | bfs | auto (bounded-frontier BFS chooser)
+    bfs_chunk: int = 32                  # level-3 candidates per frontier item
+    frontier_bytes: int | None = None    # frontier buffer bound (None: FRONTIER_BUDGET)
 
 
 def resolve_worker_count(cfg: ExecutionConfig, num_buffers: int,
@@ -145,12 +148,14 @@ def _slot_capacity(forest: PlanForest, labeled: bool, max_degree: int) -> int:
 
 
 def compile_forest(forest: PlanForest, labeled: bool, list_mode: bool, max_degree: int,
-                   flatten: bool = True, instrument: bool = False) -> CompiledPlan:
+                   flatten: bool = True, instrument: bool = False,
+                   frontier: str | None = None) -> CompiledPlan:
     """Generate + NVRTC-compile (cached by generated source)."""
     cap = _slot_capacity(forest, labeled, max_degree)
     gen = codegen.generate(forest, labeled=labeled, list_mode=list_mode,
                            smem_slot_cap=cap, warps_per_block=WARPS_PER_BLOCK,
-                           stage_words=STAGE_WORDS, flatten=flatten, instrument=instrument)
+                           stage_words=STAGE_WORDS, flatten=flatten, instrument=instrument,
+                           frontier=frontier)
     key = gen.key
     with _cache_lock:
         hit = _cache.get(key)
@@ -319,6 +324,46 @@ def _is_diamond_count(g: Graph, forest: PlanForest, tasks, sink, index, rr) -> b
     return isinstance(tasks, VertexTasks)
 
 
+FRONTIER_BUDGET = 16 << 30      # bytes of level-3 frontier items kept in HBM at once
+FRONTIER_ITEM = 16              # bytes per item (G2MItem)
+SKEW_FOR_BFS = 8.0              # max degree / average degree that makes DFS lopsided
+
+
+def choose_search(g: Graph, forest: PlanForest, tasks, cfg: ExecutionConfig | None = None,
+                  sink=None) -> tuple[str, str]:
+    """DFS or bounded-frontier BFS for one forest on one graph, with the
+    reason (the "bounded-bfs" optimisation-log line). BFS needs a level-3
+    node with children to split (edge-parallel count forests, unlabeled);
+    ``auto`` takes it when the degree distribution is skewed enough for
+    warp-per-edge DFS to be lopsided and the whole level-3 frontier fits the
+    budget: items <= nodes3 * (Σ_tasks d(v1) / chunk + tasks) with
+    Σ_tasks d(v1) <= Σ_v d(v)^2 (SURVEY A.5 sizes it exactly for 4-motifs)."""
+    cfg = cfg or ExecutionConfig()
+    mode = cfg.search
+    if mode not in ("auto", "dfs", "bfs"):
+        raise ValueError(f"unknown search strategy {mode!r}")
+    n3 = codegen.frontier_nodes(forest)
+    if mode == "dfs":
+        return "dfs", "depth-first search requested"
+    if n3 == 0 or not isinstance(tasks, EdgeTaskList) or g.labels is not None \
+            or (sink is not None and _has_emitters(forest)):
+        return "dfs", "no level-3 subtree to split (or list/labeled/vertex tasks)"
+    deg = np.diff(np.asarray(g.row_offsets, dtype=np.int64))
+    sq = float(np.dot(deg, deg)) if len(deg) else 0.0
+    items = n3 * (sq / max(cfg.bfs_chunk, 1) + len(tasks))
+    est = int(items * FRONTIER_ITEM)
+    budget = cfg.frontier_bytes or FRONTIER_BUDGET
+    if mode == "bfs":
+        return "bfs", f"bounded-frontier BFS requested (frontier <= {est} B, blocks of <= {budget} B)"
+    avg = g.num_edges / max(g.num_vertices, 1)
+    skew = g.max_degree / max(avg, 1e-9)
+    if skew < SKEW_FOR_BFS:
+        return "dfs", f"degree skew {skew:.1f} < {SKEW_FOR_BFS}: DFS is balanced"
+    if est > budget:
+        return "dfs", f"level-3 frontier <= {est} B exceeds the {budget} B budget"
+    return "bfs", f"level-3 frontier <= {est} B fits the {budget} B budget; degree skew {skew:.1f}"
+
+
 def _has_emitters(forest: PlanForest) -> bool:
     return any(a == EMIT_MATCH for r in forest.roots for n in iter_nodes(r)
                for a, _ in n.actions.values())
@@ -326,7 +371,8 @@ def _has_emitters(forest: PlanForest) -> bool:
 
 def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None = None,
             rr=None, index=None, flatten: bool = True, run_config: N.RunConfig | None = None,
-            instrument: bool = False, lgs: bool = True):
+            instrument: bool = False, lgs: bool = True, search: str = "dfs",
+            cfg: ExecutionConfig | None = None):
     """Run one forest on one GPU. Returns (counts, RunStats, stopped, compile)."""
     dev = N.default_device() if device is None else device
     N.require_device(dev)
@@ -371,6 +417,24 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
             return {pid: int(words[0]) | (int(words[1]) << 64)}, stats, False, None
         if rc != N.G2M_EUSAGE:          # out-degree beyond the tiers: generated kernel below
             N.check(rc, "diamond")
+    if search != "dfs" and not instrument and index is None:
+        ecfg = cfg or ExecutionConfig()
+        if search == "bfs" or ecfg.search != search:
+            ecfg = ExecutionConfig(**{**ecfg.__dict__, "search": search})
+        if choose_search(g, forest, tasks, ecfg, sink)[0] == "bfs":
+            ce = compile_forest(forest, labeled, False, dg.max_degree, flatten=flatten,
+                                frontier="expand")
+            cc = compile_forest(forest, labeled, False, dg.max_degree, flatten=flatten,
+                                frontier="consume")
+            spec, keep = task_spec(tasks, rr=rr)
+            words = np.zeros(2 * max(ce.gen.num_patterns, 1), dtype=np.uint64)
+            stats = N.RunStats()
+            rcfg = run_config if run_config is not None else N.RunConfig()
+            N.check(N.lib().g2m_run_bfs(ce.handle, cc.handle, dg.handle, C.byref(spec), C.byref(rcfg),
+                                        int(ecfg.bfs_chunk), int(ecfg.frontier_bytes or FRONTIER_BUDGET),
+                                        N.ptr(words, C.c_uint64), C.byref(stats)), "bfs")
+            del keep
+            return _counts_from(words, ce.gen.pattern_ids), stats, False, ce
     list_mode = sink is not None and _has_emitters(forest)
     cp = compile_forest(forest, labeled, list_mode, dg.max_degree, flatten=flatten,
                         instrument=instrument)
@@ -444,7 +508,8 @@ def run_dfs(g: Graph, forest, tasks=None, cfg: ExecutionConfig | None = None,
     num_tasks = len(tasks)
     workers = resolve_worker_count(cfg, forest.num_buffers, g.max_degree, num_tasks)
     t0 = time.perf_counter()
-    counts, st, stopped, _ = execute(g, forest, tasks, sink=sink, device=device)
+    counts, st, stopped, _ = execute(g, forest, tasks, sink=sink, device=device,
+                                     search=cfg.search, cfg=cfg)
     for pid in forest.pattern_ids:
         counts.setdefault(pid, 0)
     high = tuple(int(st.high_water[i]) if i < 8 else 0 for i in range(forest.num_buffers))
@@ -508,5 +573,5 @@ def describe_kernel(forest, labeled: bool = False, list_mode: bool = False,
 
 
 __all__ = ["BudgetError", "ExecutionConfig", "ExecStats", "RunResult", "StopSearch",
-           "WorkerContext", "merge_results", "resolve_worker_count", "run_dfs",
+           "WorkerContext", "merge_results", "resolve_worker_count", "run_dfs", "choose_search",
            "run_dfs_lgs", "emit_source", "execute", "compile_forest", "VertexTasks"]

@@ -440,3 +440,44 @@ def test_diamond_support_kernels_match_generic_and_oracle():
     assert pm.subgraph_listing(complete(40), diamond(), mode="count").counts["diamond"] == 6 * comb(40, 4)
     g = GR.from_edges(G.rmat_edges(12, 16, 1), num_vertices=1 << 12)
     assert pm.subgraph_listing(g, diamond(), mode="count").counts["diamond"] == 57343012
+
+
+@pytest.mark.parametrize("chunk,fbytes", [(1, None), (7, None), (32, None), (32, 4096)])
+def test_bounded_bfs_equals_dfs(chunk, fbytes):
+    """The bounded-frontier BFS runtime (expand/consume kernels, blocks
+    redone on frontier overflow) gives the DFS counts for every forest with
+    a level-3 subtree: 4-motifs (fused), 4-cycle, diamond list plan,
+    5-cycle; explicit shuffled tasks too (reference BFS/DFS agreement,
+    test_executor.py:228-235)."""
+    graphs = [er(60, 0.2, 3), GR.from_edges(G.powerlaw_edges(3000, 4, 3), num_vertices=3000),
+              GR.from_edges(G.rmat_edges(10, 8, 2), num_vertices=1 << 10)]
+    forests = [PL.fuse_multi_pattern([make_plan(p, rewrite=True) for p in P.generate_all_motifs(4)]),
+               PL.as_forest(make_plan(cycle4())),
+               PL.as_forest(make_plan(diamond(), mode="list")),
+               PL.as_forest(make_plan(P.Pattern(5, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0)])))]
+    cfg = EX.ExecutionConfig(search="bfs", bfs_chunk=chunk, frontier_bytes=fbytes)
+    for g in graphs:
+        for f in forests:
+            tasks = EX._default_tasks(g, f)
+            want, _, _, _ = EX.execute(g, f, tasks, lgs=False)
+            got, st, _, _ = EX.execute(g, f, tasks, lgs=False, search="bfs", cfg=cfg)
+            assert got == want, (g, f.pattern_ids)
+            if fbytes:
+                assert st.high_water[6] > 1       # ran in several bounded blocks
+    g = graphs[1]
+    f = forests[0]
+    tasks = GR.EdgeTaskList(GR.all_edge_tasks(g), reduced=False)
+    perm = np.random.default_rng(1).permutation(len(tasks.edges))
+    shuffled = GR.EdgeTaskList(tasks.edges[perm], reduced=False)
+    want = EX.execute(g, f, shuffled, lgs=False)[0]
+    assert EX.execute(g, f, shuffled, lgs=False, search="bfs", cfg=cfg)[0] == want
+
+
+def test_kmotif_bfs_log_and_counts():
+    g = GR.from_edges(G.powerlaw_edges(20000, 4, 3), num_vertices=20000)
+    res = pm.run_job(pm.MiningJob(graph=g, patterns=P.generate_all_motifs(4), granularity="edge"))
+    assert res.applied("bounded-bfs")
+    dfs = pm.run_job(pm.MiningJob(graph=g, patterns=P.generate_all_motifs(4), granularity="edge",
+                                  cfg=EX.ExecutionConfig(search="dfs")))
+    assert not dfs.applied("bounded-bfs")
+    assert res.counts == dfs.counts

@@ -69,3 +69,39 @@ def test_no_gpu_path_raises():
     import paper_2112_09761_b200 as pm
     with pytest.raises(N.NativeUnavailable):
         pm.triangle_count(G.complete(4))
+
+
+@pytest.mark.parametrize("name", ["4-motif", "4-cycle", "diamond-list", "5-clique"])
+def test_nvrtc_compiles_frontier_kernels(name):
+    """The bounded-frontier BFS expand/consume pair compiles for every forest
+    with a level-3 subtree (and is refused for the others)."""
+    forest = _forests()[name]
+    if EX.codegen.frontier_nodes(forest) == 0 or forest.uses_orientation:
+        pytest.skip("no level-3 subtree on an edge-parallel forest")
+    for fr in ("expand", "consume"):
+        cp = EX.compile_forest(forest, labeled=False, list_mode=False, max_degree=1000, frontier=fr)
+        assert cp.handle
+    with pytest.raises(ValueError):
+        EX.codegen.generate(forest, labeled=True, frontier="expand")
+
+
+def test_search_chooser():
+    import graphs as G
+    g = G.er(60, 0.2, 3)
+    plans = [make_plan(p, rewrite=True) for p in P.generate_all_motifs(4)]
+    f = PL.fuse_multi_pattern(plans)
+    tasks = EX._default_tasks(g, f)
+    assert EX.choose_search(g, f, tasks, EX.ExecutionConfig(search="dfs"))[0] == "dfs"
+    assert EX.choose_search(g, f, tasks, EX.ExecutionConfig(search="bfs"))[0] == "bfs"
+    # ER is not skewed: auto keeps DFS
+    assert EX.choose_search(g, f, tasks)[0] == "dfs"
+    from paper_2112_09761_b200 import graph as GRM
+    hub = GRM.from_edges([(0, i) for i in range(1, 400)] + [(i, i + 1) for i in range(1, 399)],
+                         num_vertices=400)          # max degree 399 >> average 4
+    assert EX.choose_search(hub, f, EX._default_tasks(hub, f))[0] == "bfs"
+    assert EX.choose_search(hub, f, EX._default_tasks(hub, f),
+                            EX.ExecutionConfig(frontier_bytes=64))[0] == "dfs"
+    tc = PL.as_forest(make_plan(P.generate_clique(3), oriented=True))
+    assert EX.choose_search(g, tc, EX._default_tasks(g, tc))[0] == "dfs"
+    with pytest.raises(ValueError):
+        EX.choose_search(g, f, tasks, EX.ExecutionConfig(search="nope"))
