@@ -246,6 +246,7 @@ def main():
     kind, warg, _, desc = WORKLOADS[args.workload]
     os.environ["G2M_DEVICE"] = str(local)
     import paper_2112_09761_b200 as pm
+    from paper_2112_09761_b200 import distributed as D
     from paper_2112_09761_b200 import executor as EX
 
     spec = graph_spec(args)
@@ -296,7 +297,7 @@ def main():
         return
 
     # ------------------------------------------------------------------ b200
-    rr = (256, world, rank) if world > 1 else None
+    rr = D.shard(rank, world)
 
     def step():   # run_job's search choice (DFS / bounded-frontier BFS), logged as "bounded-bfs"
         counts, st, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, search="auto")
@@ -321,16 +322,10 @@ def main():
     clocks = sampler.stop()
     my_ms = float(np.mean(dev_ms))
     total_counts = counts
-    if dist is not None:
-        import torch
-        t = torch.tensor([my_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        c = torch.tensor([[v & 0xFFFFFFFF, v >> 32] for v in counts.values()], dtype=torch.int64,
-                         device=f"cuda:{local}")
-        dist.all_reduce(c)
-        total_counts = {k: int(c[i, 0].item()) + (int(c[i, 1].item()) << 32)
-                        for i, k in enumerate(counts)}
+    if dist is not None:   # the job's time is its slowest rank; counts add up exactly
+        dev = f"cuda:{local}"
+        ms = D.allreduce_max(my_ms, device=dev)
+        total_counts = D.allreduce_counts(counts, device=dev)
     else:
         ms = my_ms
     value = E / (ms / 1000.0)
@@ -358,10 +353,7 @@ def main():
                 e2e_s.append(dt)
         e_ms = float(np.mean(e2e_s)) * 1000.0
         if dist is not None:
-            import torch
-            t = torch.tensor([e_ms], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+            e_ms = D.allreduce_max(e_ms, device=f"cuda:{local}")
         e2e = {"value": E / (e_ms / 1000.0), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(16 * len(counts) + 8 * 32), "ms_per_step": e_ms,
                "path": "public API (pm.k_clique / triangle_count / subgraph_listing / k_motif) on a "

@@ -1,0 +1,98 @@
+"""Multi-process path on CPU (gloo, world size 2): the chunked round-robin
+shares that bench.py / run_on_devices hand to each GPU partition the task
+list, per-rank counts add up to the whole count, and the 128-bit count
+reduction is exact. The per-rank mining here is the CPU oracle (test
+infrastructure); on GPUs it is the same share run by the kernels."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import graphs as G
+from oracle import oracle as O
+from paper_2112_09761_b200 import distributed as D
+from paper_2112_09761_b200 import graph as GR
+from paper_2112_09761_b200 import plan as PL
+from paper_2112_09761_b200 import scheduler
+from util import cycle4, diamond, make_plan, orient_host
+
+from paper_2112_09761_b200 import pattern as P
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _edge_tasks(g):
+    off = np.asarray(g.row_offsets, dtype=np.int64)
+    src = np.repeat(np.arange(g.num_vertices, dtype=np.int64), np.diff(off))
+    return np.column_stack([src, g.neighbors.astype(np.int64)])
+
+
+def _worker(rank, world, port, results):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        chunk, parts, part = D.shard(rank, world, chunk=16)
+        g = GR.from_edges(G.rmat_edges(10, 8, 3), num_vertices=1 << 10)
+        out = {}
+        # edge-task share (generated plan kernels): implicit list, chunked RR
+        for name, gg, f in [
+            ("diamond", g, PL.as_forest(make_plan(diamond(), g, rewrite=True))),
+            ("4-cycle", g, PL.as_forest(make_plan(cycle4(), g))),
+        ]:
+            all_t = _edge_tasks(gg)
+            q = scheduler.split_chunked_rr(np.arange(len(all_t)), parts, 1, alpha=chunk).queues[part]
+            mine, _ = O.run(gg, f, tasks=all_t[q], edge=True)
+            out[name] = D.allreduce_counts(mine)
+        # source-vertex share (LGS clique / wedge kernels): (v // chunk) % parts == part
+        og = orient_host(g)
+        f4 = PL.as_forest(make_plan(P.generate_clique(4), g, oriented=True))
+        all_t = _edge_tasks(og)
+        keep = (all_t[:, 0] // chunk) % parts == part
+        mine, _ = O.run(og, f4, tasks=all_t[keep], edge=True)
+        out["4-clique"] = D.allreduce_counts(mine)
+        # exact 128-bit reduction
+        out["big"] = D.allreduce_counts({"a": (1 << 100) + rank, "b": (1 << 64) - 1, "c": 0})
+        out["max"] = D.allreduce_max(1.5 + rank)
+        results[rank] = out
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_shards_and_reduction():
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    assert set(results.keys()) == {0, 1}
+    g = GR.from_edges(G.rmat_edges(10, 8, 3), num_vertices=1 << 10)
+    want = {
+        "diamond": O.run(g, PL.as_forest(make_plan(diamond(), g, rewrite=True)))[0],
+        "4-cycle": O.run(g, PL.as_forest(make_plan(cycle4(), g)))[0],
+        "4-clique": O.run(orient_host(g), PL.as_forest(make_plan(P.generate_clique(4), g,
+                                                                  oriented=True)))[0],
+    }
+    for r in range(world):
+        res = results[r]
+        for k, v in want.items():
+            assert res[k] == v, (r, k)
+        assert res["big"] == {"a": (1 << 101) + 1, "b": 2 * ((1 << 64) - 1), "c": 0}
+        assert res["max"] == 2.5
+
+
+def test_shard_and_limbs():
+    assert D.shard(0, 1) is None
+    assert D.shard(3, 8) == (256, 8, 3)
+    with pytest.raises(ValueError):
+        D.shard(8, 8)
+    for v in (0, 1, (1 << 32) - 1, 1 << 64, (1 << 128) - 1):
+        assert D.from_limbs(D.to_limbs(v)) == v
+    with pytest.raises(ValueError):
+        D.to_limbs(1 << 128)
