@@ -58,7 +58,7 @@
 extern "C" {
 #endif
 
-#define G2M_ABI_VERSION 2
+#define G2M_ABI_VERSION 3
 
 #define G2M_OK 0
 #define G2M_EUSAGE 1
@@ -92,6 +92,7 @@ typedef struct g2m_graph_info {
     int32_t labeled;
     int32_t device;
     int32_t reserved;
+    uint64_t sum_degree_sq; /* Σ_v degree(v)^2 (frontier bound of the BFS runtime) */
 } g2m_graph_info;
 
 typedef struct g2m_task_spec {
@@ -169,6 +170,9 @@ int g2m_graph_info_get(const g2m_graph* g, g2m_graph_info* info);
 int g2m_graph_download(const g2m_graph* g, uint64_t* row_offsets, uint32_t* neighbors,
                        uint32_t* labels_or_null);
 int g2m_graph_destroy(g2m_graph* g);
+/* len(EdgeTaskList.implicit(g, reduced=True)) (graph.py:270-286): slots with
+ * dst < src, counted on the device (cached with the reduced task offsets). */
+int g2m_graph_reduced_tasks(const g2m_graph* g, uint64_t* out);
 
 int g2m_kernel_compile(const char* cuda_source, const char* kernel_name,
                        const char* const* header_sources, const char* const* header_names,

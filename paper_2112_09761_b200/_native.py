@@ -17,7 +17,7 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libg2m.so"
 DEVICE_HEADER = PKG_DIR / "csrc" / "g2m_device.cuh"
 
-ABI_VERSION = 2                     # G2M_ABI_VERSION in include/g2m.h
+ABI_VERSION = 3                     # G2M_ABI_VERSION in include/g2m.h
 G2M_OK, G2M_EUSAGE, G2M_EBUDGET, G2M_ECUDA, G2M_STOPPED = 0, 1, 2, 3, 4
 TASKS_EDGE, TASKS_VERTEX = 0, 1
 SRC_IMPLICIT, SRC_PAIRS, SRC_VERTICES, SRC_INDEX = 0, 1, 2, 3
@@ -26,7 +26,8 @@ SRC_IMPLICIT, SRC_PAIRS, SRC_VERTICES, SRC_INDEX = 0, 1, 2, 3
 class GraphInfo(C.Structure):
     _fields_ = [("num_vertices", C.c_uint64), ("num_slots", C.c_uint64),
                 ("max_degree", C.c_uint64), ("oriented", C.c_int32),
-                ("labeled", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32)]
+                ("labeled", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32),
+                ("sum_degree_sq", C.c_uint64)]
 
 
 class TaskSpec(C.Structure):
@@ -86,6 +87,7 @@ SIGNATURES = {
     "g2m_graph_info_get": (C.c_int, [_P, C.POINTER(GraphInfo)]),
     "g2m_graph_download": (C.c_int, [_P, _u64p, _u32p, _u32p]),
     "g2m_graph_destroy": (C.c_int, [_P]),
+    "g2m_graph_reduced_tasks": (C.c_int, [_P, _u64p]),
     "g2m_kernel_compile": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_char_p),
                                      C.POINTER(C.c_char_p), C.c_int32,
                                      C.POINTER(KernelMeta), C.POINTER(_P)]),

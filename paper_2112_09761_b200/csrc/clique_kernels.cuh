@@ -104,16 +104,13 @@ __device__ __forceinline__ u32 probe_rows(const u64* __restrict__ off, const u32
     fl_base[lane] = ro - (u64)(incl - rn);     // nbr index of flattened position e = base + e
     __syncwarp();
     u32 hits = 0;
-    u32 ow = 0;
-    for (u32 e = lane; e < tot; e += 32) {
-        while (fl_end[ow] <= e) ++ow;
-        const u64 xi = fl_base[ow] + e;
-        const u32 x = __ldg(nbr + xi);
+    u32 ow = 0;   // this lane's owner row, monotone
+    auto one = [&](u32 o, u64 xi, u32 x) {
         if constexpr (SUP) {
             const u32 pos = P.get(x);
             if (pos != G2M_EMPTY) {
                 atomicAdd(S.t + xi, 1u);
-                atomicAdd(S.row + fl_row[ow], 1u);
+                atomicAdd(S.row + fl_row[o], 1u);
                 atomicAdd(S.col + pos, 1u);
             }
         } else if constexpr (K == 3) {
@@ -121,8 +118,29 @@ __device__ __forceinline__ u32 probe_rows(const u64* __restrict__ off, const u32
         } else {
             const u32 pos = P.get(x);
             if (pos != G2M_EMPTY)   // 32-bit halves: native ATOMS.OR (64-bit would be a CAS loop)
-                atomicOr((u32*)(R + (u64)fl_row[ow] * Ws) + (pos >> 5), 1u << (pos & 31u));
+                atomicOr((u32*)(R + (u64)fl_row[o] * Ws) + (pos >> 5), 1u << (pos & 31u));
         }
+    };
+    // two elements per lane per step: both loads are in flight before either probe
+    for (u32 e0 = 0; e0 < tot; e0 += 64) {
+        const u32 ea = e0 + lane, eb = ea + 32;
+        u32 oa = ow, ob;
+        u64 ia = 0, ib = 0;
+        u32 xa = 0, xb = 0;
+        if (ea < tot) {
+            while (fl_end[oa] <= ea) ++oa;
+            ia = fl_base[oa] + ea;
+            xa = __ldg(nbr + ia);
+        }
+        ob = oa;
+        if (eb < tot) {
+            while (fl_end[ob] <= eb) ++ob;
+            ib = fl_base[ob] + eb;
+            xb = __ldg(nbr + ib);
+        }
+        if (ea < tot) one(oa, ia, xa);
+        if (eb < tot) one(ob, ib, xb);
+        ow = ob;
     }
     __syncwarp();
     return hits;
@@ -245,24 +263,73 @@ __host__ __device__ constexpr size_t cta_smem_bytes(int K, int W, int NW, u32 bm
     return (GR ? 0 : (size_t)8 * cta_row_words(K, W, NW))        // R, T
            + (SUP ? (size_t)4 * 2 * 64 * W : 0)                  // support row / column counters
            + (size_t)8 * 64 * W                                  // RB
-           + (size_t)4 * 64 * W * 2 + (size_t)4 * 2 * W          // A, RE, BT
+           + (size_t)4 * 64 * W * 3 + (size_t)4 * 2 * W          // A, RE, LR, BT
            + (size_t)4 * 256 * W                                 // hash keys + vals
            + (size_t)NW * 4 * cta_warp_words(K)                  // per-warp scratch
            + (size_t)4 * bmw + (size_t)2 * ((bmw + 1) & ~1u);    // bitmap, pre
 }
 
-// CTA-wide flattened probe of all out-lists N+(A[i]), i < d: the warps
-// stride over the concatenation in 64-element steps (every warp gets the
-// same number of elements, whatever the row lengths). RE[i] is the
-// inclusive end of row i in the concatenation, RB[i] the nbr index of its
-// position 0. K == 3 counts members; otherwise sets the row bits of R.
+// Rows with at least kLongRow candidates are probed row by row (a warp per
+// row, lanes striding, no owner search); the rest are concatenated.
+constexpr u32 kLongRow = 128;
+
+// One probed element x (nbr index xi) of row `row` of source A.
+template <int K, bool SUP, typename Probe>
+__device__ __forceinline__ void probe_one(u32 row, u64 xi, u32 x, u64* R, u32 Ws, const Probe& P,
+                                          const Support& S, u32& hits) {
+    if constexpr (SUP) {
+        const u32 pos = P.get(x);
+        if (pos != G2M_EMPTY) {
+            atomicAdd(S.t + xi, 1u);
+            atomicAdd(S.row + row, 1u);
+            atomicAdd(S.col + pos, 1u);
+        }
+    } else if constexpr (K == 3) {
+        hits += P.has(x) ? 1u : 0u;
+    } else {
+        const u32 pos = P.get(x);
+        if (pos != G2M_EMPTY)   // 32-bit halves: native ATOMS.OR (64-bit would be a CAS loop)
+            atomicOr((u32*)(R + (u64)row * Ws) + (pos >> 5), 1u << (pos & 31u));
+    }
+}
+
+// CTA-wide probe of all out-lists N+(A[i]), i < d. Long rows (list LR,
+// nlong entries) go first, one warp per row in dynamic grabs; then the warps
+// take 64-element steps of the concatenation of the short rows in dynamic
+// grabs (RE[i]: inclusive end of row i in the concatenation, 0-length for
+// long rows; RB[i]: nbr index of its position 0). K == 3 counts members;
+// otherwise sets the row bits of R.
 template <int K, int NW, bool SUP, typename Probe>
-__device__ __forceinline__ u32 cta_probe(const u32* __restrict__ nbr, const u32* RE, const u64* RB, u32 d,
-                                         u32 tot, u32 w, u64* R, u32 Ws, const Probe& P, const Support& S) {
+__device__ __forceinline__ u32 cta_probe(const u64* __restrict__ off, const u32* __restrict__ nbr,
+                                         const u32* A, const u32* RE, const u64* RB, const u32* LR, u32 nlong,
+                                         u32 alast, u32 d, u32 tot, u32* s_lrow, u32* s_flat, u64* R, u32 Ws,
+                                         const Probe& P, const Support& S) {
     const u32 lane = g2m_lane();
     u32 hits = 0;
+    for (;;) {
+        u32 k = 0;
+        if (lane == 0) k = atomicAdd(s_lrow, 1u);
+        k = __shfl_sync(G2M_FULL, k, 0);
+        if (k >= nlong) break;
+        const u32 i = LR[k];
+        const u32 v = A[i];
+        const u64 ro = __ldg(off + v);
+        u32 rn = (u32)(__ldg(off + v + 1) - ro);
+        if (__ldg(nbr + ro + rn - 1) > alast) rn = g2m_lb(nbr + ro, rn, alast + 1u);
+        for (u32 e0 = 0; e0 < rn; e0 += 64) {
+            const u32 ea = e0 + lane, eb = ea + 32;
+            const u32 xa = ea < rn ? __ldg(nbr + ro + ea) : 0u;
+            const u32 xb = eb < rn ? __ldg(nbr + ro + eb) : 0u;
+            if (ea < rn) probe_one<K, SUP>(i, ro + ea, xa, R, Ws, P, S, hits);
+            if (eb < rn) probe_one<K, SUP>(i, ro + eb, xb, R, Ws, P, S, hits);
+        }
+    }
     u32 o0 = 0;      // first row whose end is beyond the warp's first element (warp-uniform)
-    for (u32 e0 = w * 64; e0 < tot; e0 += NW * 64) {
+    for (;;) {
+        u32 e0 = 0;
+        if (lane == 0) e0 = atomicAdd(s_flat, 64u);
+        e0 = __shfl_sync(G2M_FULL, e0, 0);     // increasing per warp, so o0 only moves forward
+        if (e0 >= tot) break;
         for (;;) {   // RE is non-decreasing, so "RE[r] <= e0" holds on a prefix
             const u32 r = o0 + lane;
             const u32 n = __popc(__ballot_sync(G2M_FULL, r < d && RE[r] <= e0));
@@ -272,55 +339,29 @@ __device__ __forceinline__ u32 cta_probe(const u32* __restrict__ nbr, const u32*
         const u32 ea = e0 + lane, eb = ea + 32;
         u32 oa = o0, ob = o0;
         u32 xa = 0, xb = 0;
+        u64 ia = 0, ib = 0;
         if (ea < tot) {
             while (RE[oa] <= ea) ++oa;
-            xa = __ldg(nbr + (RB[oa] + ea));
+            ia = RB[oa] + ea;
+            xa = __ldg(nbr + ia);
         }
         if (eb < tot) {
             ob = oa;
             while (RE[ob] <= eb) ++ob;
-            xb = __ldg(nbr + (RB[ob] + eb));
+            ib = RB[ob] + eb;
+            xb = __ldg(nbr + ib);
         }
-        if constexpr (SUP) {
-            if (ea < tot) {
-                const u32 pos = P.get(xa);
-                if (pos != G2M_EMPTY) {
-                    atomicAdd(S.t + (RB[oa] + ea), 1u);
-                    atomicAdd(S.row + oa, 1u);
-                    atomicAdd(S.col + pos, 1u);
-                }
-            }
-            if (eb < tot) {
-                const u32 pos = P.get(xb);
-                if (pos != G2M_EMPTY) {
-                    atomicAdd(S.t + (RB[ob] + eb), 1u);
-                    atomicAdd(S.row + ob, 1u);
-                    atomicAdd(S.col + pos, 1u);
-                }
-            }
-        } else if constexpr (K == 3) {
-            hits += (ea < tot && P.has(xa)) ? 1u : 0u;
-            hits += (eb < tot && P.has(xb)) ? 1u : 0u;
-        } else {
-            if (ea < tot) {
-                const u32 pos = P.get(xa);
-                if (pos != G2M_EMPTY)   // 32-bit halves: native ATOMS.OR (64-bit would be a CAS loop)
-                    atomicOr((u32*)(R + (u64)oa * Ws) + (pos >> 5), 1u << (pos & 31u));
-            }
-            if (eb < tot) {
-                const u32 pos = P.get(xb);
-                if (pos != G2M_EMPTY)
-                    atomicOr((u32*)(R + (u64)ob * Ws) + (pos >> 5), 1u << (pos & 31u));
-            }
-        }
+        if (ea < tot) probe_one<K, SUP>(oa, ia, xa, R, Ws, P, S, hits);
+        if (eb < tot) probe_one<K, SUP>(ob, ib, xb, R, Ws, P, S, hits);
     }
     return hits;
 }
 
 // ---------------------------------------------------------------------------
 // CTA tier: 64 < d <= 64*W, one CTA of NW warps per source vertex, W-word
-// rows with an odd stride. Local-graph construction is one CTA-wide
-// flattened pass over all out-lists (cta_probe); rows are counted in
+// rows with an odd stride. Local-graph construction is one CTA-wide pass
+// over all out-lists (cta_probe: long rows whole, short rows concatenated);
+// rows are counted in
 // dynamic single-row grabs, so the CTA barrier does not wait on the
 // unluckiest warp. The candidates j of R_i are compacted (CH words at a
 // time) into a shared list so every lane gets a candidate; R_j has no bits
@@ -343,7 +384,8 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
     u64* RB = GR ? smem : T + (K > 3 ? NW * (W + 1) : 0);
     u32* A = (u32*)(RB + 64 * W);
     u32* RE = A + 64 * W;
-    u32* BT = RE + 64 * W;
+    u32* LR = RE + 64 * W;
+    u32* BT = LR + 64 * W;
     u32* HK = BT + 2 * W;
     u32* HV = HK + 128 * W;
     u32* scr = HV + 128 * W;
@@ -357,13 +399,16 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
     u32* L2 = L1 + 256;
     u64* t2s = T + w * (W + 1);
     __shared__ u64 s_u;
-    __shared__ u32 s_cnt, s_tot;
+    __shared__ u32 s_cnt, s_tot, s_nlong, s_lrow, s_flat;
     for (u32 x = threadIdx.x; x < bmw; x += NW * 32) BM[x] = 0;
     u64 acc = 0;
     for (;;) {
         if (threadIdx.x == 0) {
             s_u = atomicAdd(next, 1ull);
             s_cnt = 0;
+            s_nlong = 0;
+            s_lrow = 0;
+            s_flat = 0;
         }
         __syncthreads();
         const u64 t = s_u;
@@ -394,6 +439,15 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                 rn = (u32)(__ldg(off + y + 1) - ro);
                 // out-neighbours of y are > y >= A0; drop the tail beyond A_last
                 if (rn > 32 && __ldg(nbr + ro + rn - 1) > alast) rn = g2m_lb(nbr + ro, rn, alast + 1u);
+            }
+            const bool lng = rn >= kLongRow;     // probed row by row, not concatenated
+            const u32 lm = __ballot_sync(G2M_FULL, lng);
+            if (lm) {
+                u32 lb0 = 0;
+                if (lane == 0) lb0 = atomicAdd(&s_nlong, (u32)__popc(lm));
+                lb0 = __shfl_sync(G2M_FULL, lb0, 0);
+                if (lng) LR[lb0 + __popc(lm & g2m_lanemask_lt())] = i;
+                if (lng) rn = 0;
             }
             const u32 incl = g2m_scan_incl(rn);
             if (i < d) {
@@ -442,10 +496,13 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         const u32 tot = s_tot;
         u32 hits;
         const Support S{tsup, SROW, SCOL};
+        const u32 nlong = s_nlong;
         if (use_bm)
-            hits = cta_probe<K, NW, SUP>(nbr, RE, RB, d, tot, w, R, Ws, BitmapProbe{BM, PRE, a0, span}, S);
+            hits = cta_probe<K, NW, SUP>(off, nbr, A, RE, RB, LR, nlong, alast, d, tot, &s_lrow, &s_flat, R, Ws,
+                                         BitmapProbe{BM, PRE, a0, span}, S);
         else
-            hits = cta_probe<K, NW, SUP>(nbr, RE, RB, d, tot, w, R, Ws, HashProbe{HK, HV, hl, a0, alast}, S);
+            hits = cta_probe<K, NW, SUP>(off, nbr, A, RE, RB, LR, nlong, alast, d, tot, &s_lrow, &s_flat, R, Ws,
+                                         HashProbe{HK, HV, hl, a0, alast}, S);
         if constexpr (K == 3) acc += hits;
         __syncthreads();
         if constexpr (SUP)
@@ -546,16 +603,31 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                                 }
                                 __syncwarp();
                                 const u32 nz2 = __ballot_sync(G2M_FULL, lane < Wd && t2s[lane < Wd ? lane : 0] != 0ull);
-                                for (u32 c2 = 0; c2 < Wd; c2 += CH) {
-                                    if (!((nz2 >> c2) & ((1u << CH) - 1u))) continue;
-                                    const u32 n2 = compact_bits(t2s, c2, min(c2 + CH, Wd), L2);
+                                // compact t2 into L2 (u16 bit positions) 8 words per round:
+                                // lane h < 16 owns 32-bit half-word h of the round
+                                const u32* t2h = (const u32*)t2s;
+                                unsigned short* L2h = (unsigned short*)L2;
+                                for (u32 h0 = 0; h0 < 2 * Wd; h0 += 16) {
+                                    if (!((nz2 >> (h0 >> 1)) & 0xffu)) continue;
+                                    const u32 hw = h0 + lane;
+                                    u32 m = (lane < 16 && hw < 2 * Wd) ? t2h[hw] : 0u;
+                                    const u32 c = __popc(m);
+                                    const u32 incl = g2m_scan_incl(c);
+                                    const u32 n2 = __shfl_sync(G2M_FULL, incl, 31);
+                                    u32 pos = incl - c;
+                                    while (m) {
+                                        const u32 b = __ffs(m) - 1;
+                                        m &= m - 1;
+                                        L2h[pos++] = (unsigned short)(hw * 32 + b);
+                                    }
+                                    __syncwarp();
                                     for (u32 f = lane; f < n2; f += 32) {
-                                        const u32 l = L2[f];
+                                        const u32 l = L2h[f];
                                         const u64* Rl = R + (u64)l * Ws;
-                                        u32 m = nz2 & ~((1u << (l >> 6)) - 1u);   // R_l is zero below word l/64
-                                        while (m) {
-                                            const int q3 = __ffs(m) - 1;
-                                            m &= m - 1;
+                                        u32 mq = nz2 & ~((1u << (l >> 6)) - 1u);   // R_l is zero below word l/64
+                                        while (mq) {
+                                            const int q3 = __ffs(mq) - 1;
+                                            mq &= mq - 1;
                                             acc += (u64)__popcll(t2s[q3] & Rl[q3]);
                                         }
                                     }

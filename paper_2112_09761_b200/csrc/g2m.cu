@@ -151,6 +151,7 @@ struct DevState {
     DevBuf tasks_a, tasks_b, task_match, matches, cub_tmp;
     int sms = 0;
     uint64_t launches = 0;   // kernels of ours launched on this device (g2m_run_stats.launches)
+    DevBuf tmp1, tmp2;       // grow-only scratch of the preprocessing passes (rank relabelling)
     DevBuf c4slab;           // zeroed dense 4-cycle counters, one n-word slab per block
     uint64_t c4slab_words = 0, c4slab_blocks = 0;
 };
@@ -183,7 +184,7 @@ static int dev_state(int dev, DevState** out) {
 
 struct g2m_graph {
     int dev = 0;
-    uint64_t nv = 0, slots = 0, maxdeg = 0;
+    uint64_t nv = 0, slots = 0, maxdeg = 0, sumsq = 0;
     int oriented = 0;
     DevBuf off, nbr, labels;
     std::mutex mu;
@@ -197,12 +198,20 @@ struct g2m_graph {
     std::unique_ptr<g2m_graph> oriented_copy;
 };
 
+// out[0] = max degree, out[1] = Σ degree² (the BFS frontier bound, executor.choose_search)
 __global__ void k_max_degree(const u64* off, u64 nv, u64* out) {
-    u64 best = 0;
-    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x)
-        best = max(best, off[v + 1] - off[v]);
-    for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(G2M_FULL, best, o));
+    u64 best = 0, sq = 0;
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x) {
+        const u64 d = off[v + 1] - off[v];
+        best = max(best, d);
+        sq += d * d;
+    }
+    for (int o = 16; o; o >>= 1) {
+        best = max(best, __shfl_xor_sync(G2M_FULL, best, o));
+        sq += __shfl_xor_sync(G2M_FULL, sq, o);
+    }
     if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+    if ((threadIdx.x & 31) == 0 && sq) atomicAdd(out + 1, sq);
 }
 
 static int grid_for(DevState* st, uint64_t n, int threads) {
@@ -215,14 +224,17 @@ static int grid_for(DevState* st, uint64_t n, int threads) {
 
 static int finish_graph(g2m_graph* g, DevState* st) {
     DevBuf tmp;
-    G2M_TRY(tmp.ensure(8));
-    G2M_CUDA(cudaMemsetAsync(tmp.p, 0, 8, st->stream));
+    G2M_TRY(tmp.ensure(16));
+    G2M_CUDA(cudaMemsetAsync(tmp.p, 0, 16, st->stream));
     if (g->nv) {
         k_max_degree<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, tmp.as<u64>());
         G2M_CUDA(cudaGetLastError());
     }
-    G2M_CUDA(cudaMemcpyAsync(&g->maxdeg, tmp.p, 8, cudaMemcpyDeviceToHost, st->stream));
+    uint64_t h[2] = {0, 0};
+    G2M_CUDA(cudaMemcpyAsync(h, tmp.p, 16, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
+    g->maxdeg = h[0];
+    g->sumsq = h[1];
     return G2M_OK;
 }
 
@@ -282,6 +294,7 @@ extern "C" int g2m_graph_info_get(const g2m_graph* g, g2m_graph_info* info) {
     info->labeled = g->labels.p ? 1 : 0;
     info->device = g->dev;
     info->reserved = 0;
+    info->sum_degree_sq = g->sumsq;
     return G2M_OK;
 }
 
@@ -311,37 +324,47 @@ extern "C" int g2m_graph_destroy(g2m_graph* g) {
 
 // ---- orientation (graph.py:204-221): keep u->w iff (deg u, u) < (deg w, w)
 
-__device__ __forceinline__ bool orient_keep(const u64* off, u32 u, u32 w) {
-    u64 du = off[u + 1] - off[u], dw = __ldg(off + w + 1) - __ldg(off + w);
+// Degrees as u32 (a 4-byte L2-resident lookup per slot instead of two
+// random 8-byte offset loads).
+__global__ void k_degrees(const u64* off, u64 nv, u32* deg) {
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x)
+        deg[v] = (u32)(off[v + 1] - off[v]);
+}
+
+__device__ __forceinline__ bool orient_keep(u32 du, u32 u, u32 dw, u32 w) {
     return du < dw || (du == dw && u < w);
 }
 
-__global__ void k_orient_count(const u64* off, const u32* nbr, u64 nv, u64* cnt) {
+__global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u64 nv, u64* cnt) {
     const u32 lane = g2m_lane();
     for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
          u += ((u64)gridDim.x * blockDim.x) >> 5) {
-        u64 b = off[u], e = off[u + 1];
+        const u64 b = off[u], e = off[u + 1];
+        const u32 du = (u32)(e - b);
         u32 c = 0;
         for (u64 base = b; base < e; base += 32) {
-            u64 i = base + lane;
-            bool k = i < e && orient_keep(off, (u32)u, __ldg(nbr + i));
+            const u64 i = base + lane;
+            u32 x = 0;
+            if (i < e) x = __ldg(nbr + i);
+            const bool k = i < e && orient_keep(du, (u32)u, __ldg(deg + x), x);
             c += __popc(__ballot_sync(G2M_FULL, k));
         }
         if (lane == 0) cnt[u] = c;
     }
 }
 
-__global__ void k_orient_fill(const u64* off, const u32* nbr, u64 nv, const u64* noff, u32* out) {
+__global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* deg, u64 nv, const u64* noff, u32* out) {
     const u32 lane = g2m_lane();
     for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
          u += ((u64)gridDim.x * blockDim.x) >> 5) {
-        u64 b = off[u], e = off[u + 1];
+        const u64 b = off[u], e = off[u + 1];
+        const u32 du = (u32)(e - b);
         u64 w = noff[u];
         for (u64 base = b; base < e; base += 32) {
-            u64 i = base + lane;
-            u32 x = i < e ? __ldg(nbr + i) : 0u;
-            bool k = i < e && orient_keep(off, (u32)u, x);
-            u32 m = __ballot_sync(G2M_FULL, k);
+            const u64 i = base + lane;
+            const u32 x = i < e ? __ldg(nbr + i) : 0u;
+            const bool k = i < e && orient_keep(du, (u32)u, __ldg(deg + x), x);
+            const u32 m = __ballot_sync(G2M_FULL, k);
             if (k) out[w + __popc(m & g2m_lanemask_lt())] = x;
             w += __popc(m);
         }
@@ -365,11 +388,17 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     o->nv = g->nv;
     o->oriented = 1;
     G2M_TRY(o->off.ensure((g->nv + 1) * 8));
-    DevBuf cnt;
+    DevBuf& cnt = st->tmp1;   // grow-only scratch (the caller holds the device lock)
+    DevBuf& deg = st->tmp2;
     G2M_TRY(cnt.ensure(std::max<uint64_t>(g->nv, 1) * 8));
+    G2M_TRY(deg.ensure(std::max<uint64_t>(g->nv, 1) * 4));
     if (g->nv) {
+        ++st->launches;
+        k_degrees<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, deg.as<u32>());
         int grid = grid_for(st, g->nv * 32, 256);
-        k_orient_count<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), g->nv, cnt.as<u64>());
+        ++st->launches;
+        k_orient_count<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv,
+                                                      cnt.as<u64>());
         G2M_CUDA(cudaGetLastError());
     }
     G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), o->off.as<u64>(), g->nv));
@@ -378,7 +407,8 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     G2M_TRY(o->nbr.ensure(std::max<uint64_t>(o->slots, 1) * 4));
     if (g->nv) {
         int grid = grid_for(st, g->nv * 32, 256);
-        k_orient_fill<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), g->nv,
+        ++st->launches;
+        k_orient_fill<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv,
                                                      o->off.as<u64>(), o->nbr.as<u32>());
         G2M_CUDA(cudaGetLastError());
     }
@@ -412,6 +442,7 @@ extern "C" int g2m_graph_replicate(const g2m_graph* g, int32_t device, g2m_graph
     o->nv = g->nv;
     o->slots = g->slots;
     o->maxdeg = g->maxdeg;
+    o->sumsq = g->sumsq;
     o->oriented = g->oriented;
     G2M_TRY(o->off.ensure((g->nv + 1) * 8));
     G2M_TRY(o->nbr.ensure(std::max<uint64_t>(g->slots, 1) * 4));
@@ -571,20 +602,23 @@ __global__ void k_rank_scatter(const u64* off, const u64* sorted, u64 nv, u32* r
     }
 }
 
-__global__ void k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* roff, u32* out) {
+// (new row << rb | new column) per slot (ids < 2^rb); one radix sort puts
+// every row's columns in ascending order.
+__global__ void k_rank_keys64(const u64* off, const u32* nbr, u64 nv, const u32* rank, int rb, u64* keys) {
     const u32 lane = g2m_lane();
     for (u64 v = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; v < nv;
          v += ((u64)gridDim.x * blockDim.x) >> 5) {
         const u64 b = off[v], e = off[v + 1];
         if (b == e) continue;
-        u32* dst = out + roff[rank[v]];
-        for (u64 i = b + lane; i < e; i += 32) dst[i - b] = __ldg(rank + __ldg(nbr + i));
+        const u64 hi = (u64)rank[v] << rb;
+        for (u64 i = b + lane; i < e; i += 32) keys[i] = hi | __ldg(rank + __ldg(nbr + i));
     }
 }
 
-__global__ void k_sub_base(const u64* in, u64 n, u64 base, i64* out) {
+__global__ void k_low_bits(const u64* keys, u64 n, int rb, u32* out) {
+    const u64 mask = ((u64)1 << rb) - 1;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
-        out[i] = (i64)(in[i] - base);
+        out[i] = (u32)(keys[i] & mask);
 }
 
 static int ensure_rank(const g2m_graph* cg, DevState* st) {
@@ -592,15 +626,22 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     std::lock_guard<std::mutex> lk(g->mu);
     if (g->has_rank) return G2M_OK;
     const u64 nv = g->nv, slots = g->slots;
+    const bool dbg = getenv("G2M_DEBUG") != nullptr;
+    auto tr = Clock::now();
+    auto phase = [&](const char* what) {
+        if (!dbg) return;
+        cudaStreamSynchronize(st->stream);
+        fprintf(stderr, "[g2m] rank build %s: %.2f ms\n", what, ms_since(tr));
+        tr = Clock::now();
+    };
     G2M_TRY(g->rk_off.ensure((nv + 1) * 8));
     G2M_TRY(g->rk_nbr.ensure(std::max<u64>(slots, 1) * 4));
-    DevBuf indeg, keys, sorted, rank, rdeg, tmp;
+    DevBuf indeg, keys, sorted, rank, rdeg;
     G2M_TRY(indeg.ensure(std::max<u64>(nv, 1) * 4));
     G2M_TRY(keys.ensure(std::max<u64>(nv, 1) * 8));
     G2M_TRY(sorted.ensure(std::max<u64>(nv, 1) * 8));
     G2M_TRY(rank.ensure(std::max<u64>(nv, 1) * 4));
     G2M_TRY(rdeg.ensure(std::max<u64>(nv, 1) * 8));
-    G2M_TRY(tmp.ensure(std::max<u64>(slots, 1) * 4));
     G2M_CUDA(cudaMemsetAsync(indeg.p, 0, std::max<u64>(nv, 1) * 4, st->stream));
     if (nv) {
         if (slots && g->oriented) {   // symmetric graphs: deg = row length, no in-degree term
@@ -623,49 +664,42 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
                                                                        rank.as<u32>(), rdeg.as<u64>());
         G2M_CUDA(cudaGetLastError());
     }
+    phase("keys+sort+scatter");
     G2M_TRY(exclusive_scan_u64(st, rdeg.as<u64>(), g->rk_off.as<u64>(), nv));
     if (nv && slots) {
+        int rb = 1;
+        while (rb < 32 && ((u64)1 << rb) < nv) ++rb;
+        G2M_TRY(st->tmp1.ensure(slots * 8));   // grow-only device scratch, no malloc per call
+        G2M_TRY(st->tmp2.ensure(slots * 8));
+        u64* k64 = st->tmp1.as<u64>();
+        u64* s64 = st->tmp2.as<u64>();
         ++st->launches;
-        k_rank_fill<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), nv,
-                                                                          rank.as<u32>(), g->rk_off.as<u64>(),
-                                                                          tmp.as<u32>());
+        k_rank_keys64<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), nv,
+                                                                            rank.as<u32>(), rb, k64);
         G2M_CUDA(cudaGetLastError());
-        // sort every row; cub's segmented sort takes int item counts, so go in
-        // batches of whole rows with < 2^30 items (rows are <= max degree long)
-        std::vector<u64> hoff(nv + 1);
-        G2M_CUDA(cudaMemcpyAsync(hoff.data(), g->rk_off.p, (nv + 1) * 8, cudaMemcpyDeviceToHost, st->stream));
-        G2M_CUDA(cudaStreamSynchronize(st->stream));
-        const u64 kBatch = (u64)1 << 30;
-        DevBuf rel;
-        G2M_TRY(rel.ensure((nv + 1) * 8));
-        u64 r0 = 0;
-        while (r0 < nv) {
-            u64 r1 = std::upper_bound(hoff.begin() + r0, hoff.end(), hoff[r0] + kBatch) - hoff.begin() - 1;
-            if (r1 <= r0) r1 = r0 + 1;
-            if (r1 > nv) r1 = nv;
-            const u64 base = hoff[r0], items = hoff[r1] - base;
-            if (items) {
-                // segment offsets relative to this batch
-                ++st->launches;
-                k_sub_base<<<grid_for(st, r1 - r0 + 1, 256), 256, 0, st->stream>>>(g->rk_off.as<u64>() + r0,
-                                                                                    r1 - r0 + 1, base, rel.as<i64>());
-                G2M_CUDA(cudaGetLastError());
-                const i64* bo = rel.as<i64>();
-                const i64* eo = rel.as<i64>() + 1;
-                size_t tb = 0;
-                G2M_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, tmp.as<u32>() + base,
-                                                            g->rk_nbr.as<u32>() + base, (int)items, (int)(r1 - r0),
-                                                            bo, eo, st->stream));
-                G2M_TRY(st->cub_tmp.ensure(tb));
-                G2M_CUDA(cub::DeviceSegmentedSort::SortKeys(st->cub_tmp.p, tb, tmp.as<u32>() + base,
-                                                            g->rk_nbr.as<u32>() + base, (int)items, (int)(r1 - r0),
-                                                            bo, eo, st->stream));
-            }
-            r0 = r1;
-        }
+        phase("scan+keys");
+        size_t tb2 = 0;
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb2, k64, s64, (int64_t)slots, 0, 2 * rb, st->stream));
+        G2M_TRY(st->cub_tmp.ensure(tb2));
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(st->cub_tmp.p, tb2, k64, s64, (int64_t)slots, 0, 2 * rb, st->stream));
+        ++st->launches;
+        k_low_bits<<<grid_for(st, slots, 256), 256, 0, st->stream>>>(s64, slots, rb, g->rk_nbr.as<u32>());
+        G2M_CUDA(cudaGetLastError());
     }
     G2M_CUDA(cudaStreamSynchronize(st->stream));
+    phase("radix sort");
     g->has_rank = true;
+    return G2M_OK;
+}
+
+extern "C" int g2m_graph_reduced_tasks(const g2m_graph* g, uint64_t* out) {
+    if (!g || !out) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    G2M_TRY(ensure_reduced(g, st));
+    *out = g->red_total;
     return G2M_OK;
 }
 

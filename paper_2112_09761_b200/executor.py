@@ -324,6 +324,22 @@ def _is_diamond_count(g: Graph, forest: PlanForest, tasks, sink, index, rr) -> b
     return isinstance(tasks, VertexTasks)
 
 
+def kernel_family(g: Graph, forest: PlanForest, tasks, sink=None, index=None, rr=None,
+                  lgs: bool = True, instrument: bool = False) -> str:
+    """Which kernels ``execute`` runs for this forest: "lgs" (bitmap k-clique),
+    "cycle4" (wedge aggregation), "diamond" (edge triangle support) or
+    "plan" (the generated plan kernel, DFS or bounded BFS)."""
+    if instrument or not lgs:
+        return "plan"
+    if _lgs_clique_k(g, forest, tasks, sink, index):
+        return "lgs"
+    if _is_cycle4_count(g, forest, tasks, sink, index):
+        return "cycle4"
+    if _is_diamond_count(g, forest, tasks, sink, index, rr):
+        return "diamond"
+    return "plan"
+
+
 FRONTIER_BUDGET = 16 << 30      # bytes of level-3 frontier items kept in HBM at once
 FRONTIER_ITEM = 16              # bytes per item (G2MItem)
 SKEW_FOR_BFS = 8.0              # max degree / average degree that makes DFS lopsided
@@ -348,8 +364,9 @@ def choose_search(g: Graph, forest: PlanForest, tasks, cfg: ExecutionConfig | No
     if n3 == 0 or not isinstance(tasks, EdgeTaskList) or g.labels is not None \
             or (sink is not None and _has_emitters(forest)):
         return "dfs", "no level-3 subtree to split (or list/labeled/vertex tasks)"
-    deg = np.diff(np.asarray(g.row_offsets, dtype=np.int64))
-    sq = float(np.dot(deg, deg)) if len(deg) else 0.0
+    if mode == "auto" and kernel_family(g, forest, tasks, sink) != "plan":
+        return "dfs", f"{kernel_family(g, forest, tasks, sink)} kernels, not the plan kernel"
+    sq = float(g.sum_degree_sq())
     items = n3 * (sq / max(cfg.bfs_chunk, 1) + len(tasks))
     est = int(items * FRONTIER_ITEM)
     budget = cfg.frontier_bytes or FRONTIER_BUDGET

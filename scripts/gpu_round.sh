@@ -1,0 +1,10 @@
+# full check: GPU test suite, smoke, default bench (all keys), reference arm, other configs
+mkdir -p gpurun_out
+T=${1:-r01}
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_pytest_gpu.log 2>&1; tail -3 gpurun_out/${T}_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; tail -2 gpurun_out/${T}_smoke.log
+timeout 900 python bench.py > gpurun_out/${T}_bench_cl4.json 2> gpurun_out/${T}_bench_cl4.err; echo bench rc=$?; cut -c1-300 gpurun_out/${T}_bench_cl4.json
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${T}_bench_ref.json 2> gpurun_out/${T}_bench_ref.err; echo ref rc=$?; cut -c1-300 gpurun_out/${T}_bench_ref.json
+for w in tc cl5 c4 diamond mc3 mc4; do
+  timeout 900 python bench.py --workload $w --steps 3 --warmup 3 --cpu-seconds 10 > gpurun_out/${T}_bench_$w.json 2> gpurun_out/${T}_bench_$w.err; echo $w rc=$?; cut -c1-200 gpurun_out/${T}_bench_$w.json
+done
