@@ -15,18 +15,27 @@
 // wedges with the same ends. C(c,2) accumulates incrementally: an increment
 // that finds the old value k adds k (C(k+1,2) - C(k,2) = k). In rank space
 // N(v) ∩ [0, v1) is a prefix of the sorted row, so the wedge work is
-// Σ_{v1} Σ_{v ∈ N<(v1)} |N(v) ∩ [0, v1)| (Chiba-Nishizeki ordering).
+// Σ_{v1} Σ_{v ∈ N<(v1)} |N(v) ∩ [0, v1)| (Chiba-Nishizeki ordering). Wedge
+// ends of degree 1 (ranks below lo_x) can never close a cycle and are skipped.
 //
 // Tiers by the wedge bound W(v1) = Σ_{v ∈ N<(v1)} d(v):
-//   1: W <= 512   one warp per v1, counters in a per-warp shared hash (1024)
-//   2: W <= 8192  one CTA per v1, counters in a CTA shared hash (16384)
-//   3: larger     one CTA per v1, dense u32 counters in a per-CTA HBM slab,
-//                 cleared by a second walk over the same wedges.
+//   1: W <= 512       one warp per v1, counters in a per-warp shared hash
+//   2: W <= 8192      one CTA per v1, counters in a CTA shared hash
+//   3: W <= stage cap one CTA per v1: the wedge ends are bucketed by id range
+//                     into an HBM staging area (histogram, scan, scatter) and
+//                     each 1024-id bucket is counted by one warp in shared
+//                     memory -- streaming HBM traffic instead of random
+//                     counter updates
+//   4: larger         all blocks on one v1 at a time, dense counters shared
+//                     by the grid (n words, L2-resident), cleared by memset
 #pragma once
 
 #include "g2m_device.cuh"
 
 namespace g2m_c4 {
+
+constexpr u32 kBucketBits = 10;          // tier 3: ids per bucket = 1024 (one warp's counters)
+constexpr u32 kBucketIds = 1u << kBucketBits;
 
 // Counter table: increment the count of x, return its old value.
 __device__ __forceinline__ u32 hinc(u32* keys, u32* cnt, u32 mask, u32 x) {
@@ -42,11 +51,11 @@ __device__ __forceinline__ u32 hinc(u32* keys, u32* cnt, u32 mask, u32 x) {
     }
 }
 
-// Walk the wedges v1 - L[i] - x (x < r1) of rows [i0, i0+32) of L (all 32
-// lanes share the concatenated row prefixes) and apply f(x) to each x.
+// Walk the wedges v1 - L[i] - x (lo_x <= x < r1) of rows [i0, i0+32) of L
+// (all 32 lanes share the concatenated row segments) and apply f(x).
 template <typename F>
 __device__ __forceinline__ void wedges32(const u64* __restrict__ off, const u32* __restrict__ nbr,
-                                         const u32* L, u32 l1, u32 i0, u32 r1, u32* scratch, F&& f) {
+                                         const u32* L, u32 l1, u32 i0, u32 r1, u32 lo_x, u32* scratch, F&& f) {
     const u32 lane = g2m_lane();
     u32* fl_end = scratch;
     u64* fl_base = (u64*)(scratch + 32);
@@ -57,7 +66,10 @@ __device__ __forceinline__ void wedges32(const u64* __restrict__ off, const u32*
         const u32 v = L[i];
         ro = __ldg(off + v);
         const u32 dv = (u32)(__ldg(off + v + 1) - ro);
-        rn = (dv && __ldg(nbr + ro + dv - 1) < r1) ? dv : g2m_lb(nbr + ro, dv, r1);
+        const u32 s0 = (dv && __ldg(nbr + ro) < lo_x) ? g2m_lb(nbr + ro, dv, lo_x) : 0u;
+        const u32 e1 = (dv && __ldg(nbr + ro + dv - 1) < r1) ? dv : g2m_lb(nbr + ro, dv, r1);
+        rn = e1 > s0 ? e1 - s0 : 0u;
+        ro += s0;
     }
     const u32 incl = g2m_scan_incl(rn);
     const u32 tot = __shfl_sync(G2M_FULL, incl, 31);
@@ -65,18 +77,45 @@ __device__ __forceinline__ void wedges32(const u64* __restrict__ off, const u32*
     fl_base[lane] = ro - (u64)(incl - rn);
     __syncwarp();
     u32 ow = 0;
-    for (u32 e = lane; e < tot; e += 32) {
-        while (fl_end[ow] <= e) ++ow;
-        f(__ldg(nbr + (fl_base[ow] + e)));
+    for (u32 e0 = 0; e0 < tot; e0 += 64) {   // two elements per lane in flight
+        const u32 ea = e0 + lane, eb = ea + 32;
+        u32 xa = 0, xb = 0;
+        if (ea < tot) {
+            while (fl_end[ow] <= ea) ++ow;
+            xa = __ldg(nbr + (fl_base[ow] + ea));
+        }
+        if (eb < tot) {
+            u32 ob = ow;
+            while (fl_end[ob] <= eb) ++ob;
+            xb = __ldg(nbr + (fl_base[ob] + eb));
+            ow = ob;
+        }
+        if (ea < tot) f(xa);
+        if (eb < tot) f(xb);
     }
     __syncwarp();
+}
+
+// Row batches of L in dynamic 32-row grabs from a shared (CTA) or global
+// (grid) counter; f as in wedges32.
+template <typename F>
+__device__ __forceinline__ void wedge_rows(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* L,
+                                           u32 l1, u32 r1, u32 lo_x, u32* ctr, u32* scratch, F&& f) {
+    const u32 lane = g2m_lane();
+    for (;;) {
+        u32 i0 = 0;
+        if (lane == 0) i0 = atomicAdd(ctr, 32u);
+        i0 = __shfl_sync(G2M_FULL, i0, 0);
+        if (i0 >= l1) break;
+        wedges32(off, nbr, L, l1, i0, r1, lo_x, scratch, f);
+    }
 }
 
 // ---- tier 1: warp per v1 ---------------------------------------------------
 template <int WPB>
 __global__ void __launch_bounds__(WPB * 32)
 k_c4_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-          const u32* __restrict__ lows, u64 nverts, u64* next, u64* count) {
+          const u32* __restrict__ lows, u64 nverts, u64* next, u64* count, u32 lo_x) {
     constexpr u32 CAP = 1024;
     __shared__ u32 sK[WPB][CAP];
     __shared__ u32 sC[WPB][CAP];
@@ -97,7 +136,7 @@ k_c4_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* _
         const u32 l1 = __ldg(lows + t);
         const u32* L = nbr + __ldg(off + r1);
         for (u32 i0 = 0; i0 < l1; i0 += 32)
-            wedges32(off, nbr, L, l1, i0, r1, sScr[w], [&](u32 x) { acc += hinc(K, Cn, CAP - 1, x); });
+            wedges32(off, nbr, L, l1, i0, r1, lo_x, sScr[w], [&](u32 x) { acc += hinc(K, Cn, CAP - 1, x); });
         for (u32 x = lane; x < CAP; x += 32) { K[x] = G2M_EMPTY; Cn[x] = 0; }
         __syncwarp();
     }
@@ -105,32 +144,24 @@ k_c4_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* _
     if (lane == 0 && acc) g2m_add128(count, acc, 0);
 }
 
-// ---- tier 2/3: CTA per v1 -----------------------------------------------------
-// GLOBAL = false: counters in a shared hash of CAP entries (dynamic smem);
-// GLOBAL = true: dense counters cnt[x] in this block's HBM slab (n words).
-template <int NW, bool GLOBAL>
+// ---- tier 2: CTA per v1, shared hash of `cap` counters ----------------------
+template <int NW>
 __global__ void __launch_bounds__(NW * 32)
 k_c4_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-         const u32* __restrict__ lows, u64 nverts, u64* next, u64* count, u32* slab, u64 slab_words,
-         u32 cap) {
+         const u32* __restrict__ lows, u64 nverts, u64* next, u64* count, u32 cap, u32 lo_x) {
     extern __shared__ __align__(16) u32 smem_c4[];
-    u32* K = smem_c4;                 // shared hash keys [cap], counts [cap]   (!GLOBAL)
-    u32* Cn = K + (GLOBAL ? 0 : cap);
-    u32* scr = Cn + (GLOBAL ? 0 : cap);
-    u32* dense = slab + (u64)blockIdx.x * slab_words;
+    u32* K = smem_c4;                 // keys [cap], counts [cap], per-warp scratch [NW x 96]
+    u32* Cn = K + cap;
+    u32* wscr = Cn + cap + (threadIdx.x >> 5) * 96;
     const u32 lane = g2m_lane();
-    const u32 w = threadIdx.x >> 5;
-    u32* wscr = scr + w * 96;
     __shared__ u64 s_t;
-    __shared__ u32 s_row, s_row2;
-    if (!GLOBAL)
-        for (u32 x = threadIdx.x; x < cap; x += NW * 32) { K[x] = G2M_EMPTY; Cn[x] = 0; }
+    __shared__ u32 s_row;
+    for (u32 x = threadIdx.x; x < cap; x += NW * 32) { K[x] = G2M_EMPTY; Cn[x] = 0; }
     u64 acc = 0;
     for (;;) {
         if (threadIdx.x == 0) {
             s_t = atomicAdd(next, 1ull);
             s_row = 0;
-            s_row2 = 0;
         }
         __syncthreads();
         const u64 t = s_t;
@@ -138,27 +169,86 @@ k_c4_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __
         const u32 r1 = __ldg(verts + t);
         const u32 l1 = __ldg(lows + t);
         const u32* L = nbr + __ldg(off + r1);
-        for (;;) {
-            u32 i0 = 0;
-            if (lane == 0) i0 = atomicAdd(&s_row, 32u);
-            i0 = __shfl_sync(G2M_FULL, i0, 0);
-            if (i0 >= l1) break;
-            if (GLOBAL)
-                wedges32(off, nbr, L, l1, i0, r1, wscr, [&](u32 x) { acc += atomicAdd(dense + x, 1u); });
-            else
-                wedges32(off, nbr, L, l1, i0, r1, wscr, [&](u32 x) { acc += hinc(K, Cn, cap - 1, x); });
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row, wscr, [&](u32 x) { acc += hinc(K, Cn, cap - 1, x); });
+        __syncthreads();
+        for (u32 x = threadIdx.x; x < cap; x += NW * 32) { K[x] = G2M_EMPTY; Cn[x] = 0; }
+        __syncthreads();
+    }
+    acc = g2m_wsum(acc);
+    if (lane == 0 && acc) g2m_add128(count, acc, 0);
+}
+
+// ---- tier 3: CTA per v1, bucketed staging ------------------------------------
+// Shared memory: bucket histogram -> cursors -> bucket ends [nbmax] u32 |
+// per-warp counters [NW x 1024] u32 | per-warp scratch [NW x 96] u32.
+// stage: this block's slab of stage_cap u32 in HBM.
+__host__ __device__ constexpr size_t stage_smem_bytes(int NW, u32 nbmax) {
+    return (size_t)4 * nbmax + (size_t)4 * NW * kBucketIds + (size_t)4 * NW * 96;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32)
+k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
+           const u32* __restrict__ lows, u64 nverts, u64* next, u64* count, u32* stage_all, u64 stage_cap,
+           u32 nbmax, u32 lo_x) {
+    extern __shared__ __align__(16) u32 smem_c4[];
+    u32* H = smem_c4;
+    u32* WC = H + nbmax;
+    const u32 lane = g2m_lane();
+    const u32 w = threadIdx.x >> 5;
+    u32* wcnt = WC + w * kBucketIds;
+    u32* wscr = WC + NW * kBucketIds + w * 96;
+    u32* stage = stage_all + (u64)blockIdx.x * stage_cap;
+    __shared__ u64 s_t;
+    __shared__ u32 s_row, s_row2, s_bkt;
+    for (u32 x = lane; x < kBucketIds; x += 32) wcnt[x] = 0;
+    u64 acc = 0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            s_t = atomicAdd(next, 1ull);
+            s_row = s_row2 = s_bkt = 0;
         }
         __syncthreads();
-        if (GLOBAL) {   // clear the counters this v1 touched
-            for (;;) {
-                u32 i0 = 0;
-                if (lane == 0) i0 = atomicAdd(&s_row2, 32u);
-                i0 = __shfl_sync(G2M_FULL, i0, 0);
-                if (i0 >= l1) break;
-                wedges32(off, nbr, L, l1, i0, r1, wscr, [&](u32 x) { dense[x] = 0; });
+        const u64 t = s_t;
+        if (t >= nverts) break;
+        const u32 r1 = __ldg(verts + t);
+        const u32 l1 = __ldg(lows + t);
+        const u32* L = nbr + __ldg(off + r1);
+        const u32 nb = (r1 >> kBucketBits) + 1;
+        for (u32 b = threadIdx.x; b < nb; b += NW * 32) H[b] = 0;
+        __syncthreads();
+        // 1: histogram of the wedge ends by bucket
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row, wscr, [&](u32 x) { atomicAdd(H + (x >> kBucketBits), 1u); });
+        __syncthreads();
+        // 2: exclusive scan of the histogram (warp 0): cursors = bucket starts
+        if (w == 0) {
+            u32 carry = 0;
+            for (u32 b0 = 0; b0 < nb; b0 += 32) {
+                const u32 b = b0 + lane;
+                const u32 v = b < nb ? H[b] : 0u;
+                const u32 incl = g2m_scan_incl(v);
+                if (b < nb) H[b] = carry + incl - v;
+                carry += __shfl_sync(G2M_FULL, incl, 31);
             }
-        } else {
-            for (u32 x = threadIdx.x; x < cap; x += NW * 32) { K[x] = G2M_EMPTY; Cn[x] = 0; }
+        }
+        __syncthreads();
+        // 3: scatter the wedge ends into their buckets (cursors end as bucket ends)
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row2, wscr, [&](u32 x) {
+            stage[atomicAdd(H + (x >> kBucketBits), 1u)] = x;
+        });
+        __syncthreads();
+        // 4: one warp per bucket counts it in its private shared counters
+        for (;;) {
+            u32 b = 0;
+            if (lane == 0) b = atomicAdd(&s_bkt, 1u);
+            b = __shfl_sync(G2M_FULL, b, 0);
+            if (b >= nb) break;
+            const u32 s0 = b ? H[b - 1] : 0u, s1 = H[b];
+            if (s0 == s1) continue;
+            for (u32 e = s0 + lane; e < s1; e += 32) acc += atomicAdd(wcnt + (stage[e] & (kBucketIds - 1)), 1u);
+            __syncwarp();
+            for (u32 e = s0 + lane; e < s1; e += 32) wcnt[stage[e] & (kBucketIds - 1)] = 0;
+            __syncwarp();
         }
         __syncthreads();
     }
@@ -166,11 +256,63 @@ k_c4_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __
     if (lane == 0 && acc) g2m_add128(count, acc, 0);
 }
 
+// ---- tier 4: the whole grid on one v1, shared dense counters -----------------
+// The v1's wedges are flattened over the grid: k_c4_rows writes each row's
+// wedge count and first nbr index, a scan makes the ends, and k_c4_grid's
+// warps take 256-element steps (owner row by binary search over the ends),
+// so a few huge rows do not serialise the grid.
+__global__ void k_c4_rows(const u64* __restrict__ off, const u32* __restrict__ nbr, u32 r1, u32 l1, u32 lo_x,
+                          u64* rn_out, u64* rb_out) {
+    const u32* L = nbr + __ldg(off + r1);
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < l1; i += gridDim.x * blockDim.x) {
+        const u32 v = __ldg(L + i);
+        u64 ro = __ldg(off + v);
+        const u32 dv = (u32)(__ldg(off + v + 1) - ro);
+        const u32 s0 = (dv && __ldg(nbr + ro) < lo_x) ? g2m_lb(nbr + ro, dv, lo_x) : 0u;
+        const u32 e1 = (dv && __ldg(nbr + ro + dv - 1) < r1) ? dv : g2m_lb(nbr + ro, dv, r1);
+        rn_out[i] = e1 > s0 ? e1 - s0 : 0u;
+        rb_out[i] = ro + s0;
+    }
+}
+
+__global__ void __launch_bounds__(512)
+k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const u64* __restrict__ rb,
+          const u64* __restrict__ re, u64* ctr, u32* dense, u64* count) {
+    const u32 lane = g2m_lane();
+    const u64 tot = re[l1 - 1];
+    u64 acc = 0;
+    for (;;) {
+        u64 e0 = 0;
+        if (lane == 0) e0 = atomicAdd(ctr, 256ull);
+        e0 = __shfl_sync(G2M_FULL, e0, 0);
+        if (e0 >= tot) break;
+        // owner of e0: first row with end > e0
+        u32 lo = 0, n = l1;
+        while (n > 0) {
+            const u32 h = n >> 1;
+            if (__ldg(re + lo + h) <= e0) { lo += h + 1; n -= h + 1; } else n = h;
+        }
+        u32 ow = lo;
+#pragma unroll 2
+        for (u32 k = 0; k < 256; k += 32) {
+            const u64 e = e0 + k + lane;
+            if (e < tot) {
+                while (__ldg(re + ow) <= e) ++ow;
+                const u64 start = __ldg(re + ow) - __ldg(rn + ow);
+                const u32 x = __ldg(nbr + __ldg(rb + ow) + (e - start));
+                acc += atomicAdd(dense + x, 1u);
+            }
+        }
+    }
+    acc = g2m_wsum(acc);
+    if (lane == 0 && acc) g2m_add128(count, acc, 0);
+}
+
 // Per v1 (rank r, this partition): l1 = |N(r) ∩ [0, r)| and the wedge bound
-// W = Σ_{v ∈ N<(r)} d(v); class 1..3 as above (0: l1 < 2, no cycle).
+// W = Σ_{v ∈ N<(r)} d(v); class 1..4 as above (0: l1 < 2, no cycle).
 // One warp per vertex.
 __global__ void k_c4_bucket(const u64* off, const u32* nbr, u64 nv, u64 rr_chunk, u32 parts, u32 part,
-                            u32* lists, u32* lows, u64* wkeys, u64 stride, u64* sizes) {
+                            u64 stage_cap, u32* lists, u32* lows, u64* wkeys, u64 stride, u64* sizes) {
     const u32 lane = g2m_lane();
     for (u64 r = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; r < nv;
          r += ((u64)gridDim.x * blockDim.x) >> 5) {
@@ -186,11 +328,12 @@ __global__ void k_c4_bucket(const u64* off, const u32* nbr, u64 nv, u64 rr_chunk
         }
         wsum = g2m_wsum(wsum);
         if (lane == 0) {
-            const int c = wsum <= 512 ? 1 : (wsum <= 8192 ? 2 : 3);
+            const int c = wsum <= 512 ? 1 : (wsum <= 8192 ? 2 : (wsum <= stage_cap ? 3 : 4));
             const u64 slot = atomicAdd(sizes + c, 1ull);
             lists[(u64)c * stride + slot] = (u32)r;
             lows[(u64)c * stride + slot] = l1;
-            if (c == 3) wkeys[slot] = ((u64)(0xffffffffu - (u32)min(wsum, 0xffffffffull)) << 32) | r;   // descending W (LPT order)
+            if (c == 3)   // descending W (LPT order)
+                wkeys[slot] = ((u64)(0xffffffffu - (u32)min(wsum, 0xffffffffull)) << 32) | r;
         }
     }
 }

@@ -152,8 +152,7 @@ struct DevState {
     int sms = 0;
     uint64_t launches = 0;   // kernels of ours launched on this device (g2m_run_stats.launches)
     DevBuf tmp1, tmp2;       // grow-only scratch of the preprocessing passes (rank relabelling)
-    DevBuf c4slab;           // zeroed dense 4-cycle counters, one n-word slab per block
-    uint64_t c4slab_words = 0, c4slab_blocks = 0;
+    DevBuf c4slab;           // 4-cycle staging slabs, one per block
 };
 
 static std::mutex g_dev_mu;
@@ -194,6 +193,7 @@ struct g2m_graph {
     // the same graph relabelled by its (degree, id) order, lazily built
     DevBuf rk_off, rk_nbr;
     bool has_rank = false;
+    uint64_t rk_deg1 = 0;    // ranks [0, rk_deg1) have degree <= 1
     // symmetric graphs: degree orientation, lazily built (diamond support)
     std::unique_ptr<g2m_graph> oriented_copy;
 };
@@ -594,6 +594,14 @@ __global__ void k_rank_keys(const u64* off, const u32* indeg, u64 nv, u64* keys)
         keys[v] = ((off[v + 1] - off[v] + (u64)indeg[v]) << 32) | v;
 }
 
+__global__ void k_count_deg_le1(const u64* keys, u64 nv, u64* out) {
+    u64 c = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nv; i += (u64)gridDim.x * blockDim.x)
+        c += (keys[i] >> 32) <= 1 ? 1 : 0;
+    c = g2m_wsum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 __global__ void k_rank_scatter(const u64* off, const u64* sorted, u64 nv, u32* rank, u64* rdeg) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nv; i += (u64)gridDim.x * blockDim.x) {
         const u32 v = (u32)sorted[i];
@@ -663,6 +671,11 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
         k_rank_scatter<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), sorted.as<u64>(), nv,
                                                                        rank.as<u32>(), rdeg.as<u64>());
         G2M_CUDA(cudaGetLastError());
+        u64* d1 = (u64*)indeg.p;    // indeg is no longer needed
+        G2M_CUDA(cudaMemsetAsync(d1, 0, 8, st->stream));
+        ++st->launches;
+        k_count_deg_le1<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(sorted.as<u64>(), nv, d1);
+        G2M_CUDA(cudaMemcpyAsync(&g->rk_deg1, d1, 8, cudaMemcpyDeviceToHost, st->stream));
     }
     phase("keys+sort+scatter");
     G2M_TRY(exclusive_scan_u64(st, rdeg.as<u64>(), g->rk_off.as<u64>(), nv));
@@ -1563,35 +1576,46 @@ extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, c
     const u64* off = g->rk_off.as<u64>();
     const u32* nbr = g->rk_nbr.as<u32>();
     const u64 nv = g->nv;
+    const u32 lo_x = (u32)g->rk_deg1;
     const bool dbg = getenv("G2M_DEBUG") != nullptr;
+    constexpr int NW = 16;
+    // tier 3 setup: bucket array in shared memory, staging slab per block
+    int max_smem = 0;
+    G2M_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->dev));
+    const u32 nbmax = (u32)((nv >> g2m_c4::kBucketBits) + 2 + 3) & ~3u;   // keeps the u64 scratch aligned
+    const size_t stage_smem = g2m_c4::stage_smem_bytes(NW, nbmax);
+    const bool tier3 = stage_smem <= (size_t)max_smem;
+    u64 stage_cap = tier3 ? ((u64)8 << 20) : 0;            // wedges per v1 staged (32 MB per block)
+    if (const char* e = getenv("G2M_C4_STAGE_CAP")) stage_cap = std::min<u64>(stage_cap, strtoull(e, nullptr, 10));
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
     G2M_TRY(st->counters.ensure(32 * 8));
     u64* ctr = st->counters.as<u64>();
     G2M_CUDA(cudaMemsetAsync(ctr, 0, 32 * 8, st->stream));
     const u64 stride = std::max<u64>(nv, 1);
-    // lists/lows: 4 classes x nv u32 each; wkeys (class 3 sort keys) 2 x nv u64
-    G2M_TRY(st->tasks_b.ensure(8 * stride * 4));
+    // lists/lows: classes 0..4 x nv u32 each; wkeys (class 3 sort keys) + sorted copy
+    G2M_TRY(st->tasks_b.ensure(10 * stride * 4));
     G2M_TRY(st->matches.ensure(2 * stride * 8));
-    G2M_TRY(st->tasks_a.ensure(4 * 8));
+    G2M_TRY(st->tasks_a.ensure(8 * 8));
     u32* lists = st->tasks_b.as<u32>();
-    u32* lows = lists + 4 * stride;
+    u32* lows = lists + 5 * stride;
     u64* wkeys = st->matches.as<u64>();
     u64* wsorted = wkeys + stride;
     u64* dsizes = st->tasks_a.as<u64>();
-    G2M_CUDA(cudaMemsetAsync(dsizes, 0, 4 * 8, st->stream));
+    G2M_CUDA(cudaMemsetAsync(dsizes, 0, 8 * 8, st->stream));
     if (nv) {
         ++st->launches;
         g2m_c4::k_c4_bucket<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(
-            off, nbr, nv, rr_chunk, parts, pt, lists, lows, wkeys, stride, dsizes);
+            off, nbr, nv, rr_chunk, parts, pt, stage_cap, lists, lows, wkeys, stride, dsizes);
         G2M_CUDA(cudaGetLastError());
     }
-    uint64_t sizes[4];
-    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, 4 * 8, cudaMemcpyDeviceToHost, st->stream));
+    uint64_t sizes[5];
+    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, 5 * 8, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     if (dbg)
-        fprintf(stderr, "[g2m] cycle4: warp %llu, cta %llu, dense %llu sources\n", (unsigned long long)sizes[1],
-                (unsigned long long)sizes[2], (unsigned long long)sizes[3]);
-    // the dense tier runs its largest wedge fans first
+        fprintf(stderr, "[g2m] cycle4: warp %llu, cta %llu, staged %llu, grid %llu sources (lo_x %u)\n",
+                (unsigned long long)sizes[1], (unsigned long long)sizes[2], (unsigned long long)sizes[3],
+                (unsigned long long)sizes[4], lo_x);
+    // the staged tier runs its largest wedge fans first
     if (sizes[3]) {
         size_t tb = 0;
         G2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, wkeys, wsorted, (int64_t)sizes[3], 0, 64, st->stream));
@@ -1627,14 +1651,13 @@ extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, c
         G2M_TRY(timed([&] {
             ++st->launches;
             kern<<<st->sms * std::max(occ, 1), WPB * 32, 0, st->stream>>>(off, nbr, lists + stride, lows + stride,
-                                                                           sizes[1], next + 0, count);
+                                                                           sizes[1], next + 0, count, lo_x);
         }));
     }
-    constexpr int NW = 16;
     if (sizes[2]) {
         const u32 cap = 16384;
         const size_t smem = (size_t)2 * cap * 4 + (size_t)NW * 96 * 4;
-        auto kern = g2m_c4::k_c4_cta<NW, false>;
+        auto kern = g2m_c4::k_c4_cta<NW>;
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
         G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
@@ -1642,35 +1665,58 @@ extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, c
         G2M_TRY(timed([&] {
             ++st->launches;
             kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + 2 * stride, lows + 2 * stride,
-                                                                 sizes[2], next + 1, count, nullptr, 0, cap);
+                                                                 sizes[2], next + 1, count, cap, lo_x);
         }));
     }
     if (sizes[3]) {
-        const size_t smem = (size_t)NW * 96 * 4;
-        auto kern = g2m_c4::k_c4_cta<NW, true>;
+        auto kern = g2m_c4::k_c4_stage<NW>;
+        G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_smem));
         int occ = 0;
-        G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
-        // one zeroed n-word counter slab per block, kept (zeroed) across calls,
-        // at most a quarter of the free HBM
-        u64 want = std::min<u64>(sizes[3], (u64)st->sms * std::max(occ, 1));
-        if (st->c4slab_words != stride || st->c4slab_blocks < want) {
-            size_t fr = 0, tot = 0;
-            cudaMemGetInfo(&fr, &tot);
-            const u64 nb = std::min<u64>(want, std::max<u64>(1, (fr + st->c4slab.bytes) / 4 / (stride * 4)));
-            if (st->c4slab_words != stride || nb > st->c4slab_blocks) {
-                st->c4slab.release();
-                G2M_TRY(st->c4slab.ensure(nb * stride * 4));
-                G2M_CUDA(cudaMemsetAsync(st->c4slab.p, 0, nb * stride * 4, st->stream));
-                st->c4slab_words = stride;
-                st->c4slab_blocks = nb;
-            }
-        }
-        const u64 grid = std::min<u64>(want, st->c4slab_blocks);
+        G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, stage_smem));
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        u64 grid = std::min<u64>(sizes[3], (u64)st->sms * std::max(occ, 1));
+        grid = std::min<u64>(grid, std::max<u64>(1, (fr + st->c4slab.bytes) / 4 / (stage_cap * 4)));
+        G2M_TRY(st->c4slab.ensure(grid * stage_cap * 4));
         G2M_TRY(timed([&] {
             ++st->launches;
-            kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + 3 * stride, lows + 3 * stride,
-                                                                 sizes[3], next + 2, count, st->c4slab.as<u32>(),
-                                                                 stride, 0);
+            kern<<<(unsigned)grid, NW * 32, stage_smem, st->stream>>>(off, nbr, lists + 3 * stride, lows + 3 * stride,
+                                                                       sizes[3], next + 2, count, st->c4slab.as<u32>(),
+                                                                       stage_cap, nbmax, lo_x);
+        }));
+    }
+    if (sizes[4]) {
+        // one v1 at a time on the whole grid, its wedges flattened over all
+        // warps; counters shared by the grid (n words, L2-resident)
+        std::vector<u32> gv(sizes[4]), gl(sizes[4]);
+        G2M_CUDA(cudaMemcpyAsync(gv.data(), lists + 4 * stride, sizes[4] * 4, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaMemcpyAsync(gl.data(), lows + 4 * stride, sizes[4] * 4, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        u32 lmax = 0;
+        for (u32 l : gl) lmax = std::max(lmax, l);
+        G2M_TRY(st->tmp1.ensure(stride * 4 + 64));
+        G2M_TRY(st->tmp2.ensure((u64)lmax * 24 + 64));
+        u32* dense = st->tmp1.as<u32>();
+        u64* rn = st->tmp2.as<u64>();
+        u64* rb = rn + lmax;
+        u64* re = rb + lmax;
+        u64* gctr = ctr + 12;
+        size_t tb = 0;
+        G2M_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, rn, re, (int64_t)lmax, st->stream));
+        G2M_TRY(st->cub_tmp.ensure(tb));
+        G2M_CUDA(cudaMemsetAsync(dense, 0, stride * 4, st->stream));
+        G2M_TRY(timed([&] {
+            for (u64 q = 0; q < sizes[4]; ++q) {
+                const u32 r1 = gv[q], l1 = gl[q];
+                ++st->launches;
+                g2m_c4::k_c4_rows<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(off, nbr, r1, l1, lo_x, rn, rb);
+                size_t t2 = tb;
+                cub::DeviceScan::InclusiveSum(st->cub_tmp.p, t2, rn, re, (int64_t)l1, st->stream);
+                cudaMemsetAsync(gctr, 0, 8, st->stream);
+                ++st->launches;
+                g2m_c4::k_c4_grid<<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rn, rb, re, gctr, dense, count);
+                cudaMemsetAsync(dense, 0, (size_t)r1 * 4, st->stream);
+            }
         }));
     }
     uint64_t h[2] = {0, 0};
@@ -1679,7 +1725,7 @@ extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, c
     G2M_CUDA(cudaEventSynchronize(st->evs1));
     counts[0] = h[0];
     counts[1] = h[1];
-    S->tasks = sizes[1] + sizes[2] + sizes[3];
+    S->tasks = sizes[1] + sizes[2] + sizes[3] + sizes[4];
     float dm = 0.f;
     cudaEventElapsedTime(&dm, st->evs0, st->evs1);
     S->device_ms = dm;

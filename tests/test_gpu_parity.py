@@ -419,6 +419,16 @@ def test_cycle4_wedge_kernels_match_generic_and_oracle():
     assert sum(parts) == 52799071
 
 
+def test_cycle4_grid_tier(monkeypatch):
+    """A small staging cap sends the large wedge fans to the grid-wide tier."""
+    g = GR.from_edges(G.rmat_edges(13, 16, 4), num_vertices=1 << 13)
+    f = PL.as_forest(make_plan(cycle4(), g))
+    tasks = EX._default_tasks(g, f)
+    want = EX.execute(g, f, tasks, lgs=False)[0]
+    monkeypatch.setenv("G2M_C4_STAGE_CAP", "20000")
+    assert EX.execute(g, f, tasks)[0] == want
+
+
 def test_diamond_support_kernels_match_generic_and_oracle():
     """g2m_diamond_count (edge triangle support over the rank-space DAG) ==
     the generated diamond plan kernel (counting rewrite) == the oracle."""
