@@ -230,6 +230,61 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
     if (lane == 0 && acc) g2m_add128(count, acc, 0);
 }
 
+// ---------------------------------------------------------------------------
+// pair tier: d <= 16, one warp per source; the local edges a -> b (a, b in A)
+// are found by testing every pair of A directly, b in N+(a) by binary search
+// -- d(d-1)/2 lane-parallel tests instead of streaming the out-lists of A,
+// which for small sources are mostly far longer than A itself.
+// ---------------------------------------------------------------------------
+template <int K, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
+               u64 nverts, u64* next, u64 grab, u64* count) {
+    __shared__ u32 sA[WPB][16];
+    __shared__ __align__(8) u64 sR[WPB][16];
+    const u32 lane = g2m_lane();
+    const u32 w = threadIdx.x >> 5;
+    u32* A = sA[w];
+    u64* R = sR[w];
+    u64 acc = 0;
+    for (;;) {
+        u64 t0 = 0;
+        if (lane == 0) t0 = atomicAdd(next, grab);
+        t0 = __shfl_sync(G2M_FULL, t0, 0);
+        if (t0 >= nverts) break;
+        const u64 t1 = min(t0 + grab, nverts);
+        for (u64 t = t0; t < t1; ++t) {
+            const u32 u = __ldg(verts + t);
+            const u64 b = __ldg(off + u);
+            const u32 d = (u32)(__ldg(off + u + 1) - b);
+            if (lane < 16) {
+                A[lane] = lane < d ? __ldg(nbr + b + lane) : 0u;
+                R[lane] = 0;
+            }
+            __syncwarp();
+            const u32 np = d * (d - 1) / 2;
+            for (u32 p = lane; p < np; p += 32) {
+                u32 i = 0, rem = p;
+                while (rem >= d - 1 - i) { rem -= d - 1 - i; ++i; }
+                const u32 j = i + 1 + rem;
+                const u32 a = A[i];
+                const u64 ao = __ldg(off + a);
+                if (g2m_has_g(nbr + ao, (u32)(__ldg(off + a + 1) - ao), A[j])) {
+                    if constexpr (K == 3) acc += 1;
+                    else atomicOr((u32*)(R + i) + (j >> 5), 1u << (j & 31u));
+                }
+            }
+            if constexpr (K > 3) {
+                __syncwarp();
+                if (lane < d) acc += Chain1<K - 2>::run(R, R[lane]);
+            }
+            __syncwarp();
+        }
+    }
+    acc = g2m_wsum(acc);
+    if (lane == 0 && acc) g2m_add128(count, acc, 0);
+}
+
 // Warp-cooperative compaction of the set bits of words[q0, q1) (shared,
 // read by broadcast) into out[] as bit positions; returns the count.
 __device__ __forceinline__ u32 compact_bits(const u64* words, u32 q0, u32 q1, u32* out) {
@@ -603,26 +658,11 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                                 }
                                 __syncwarp();
                                 const u32 nz2 = __ballot_sync(G2M_FULL, lane < Wd && t2s[lane < Wd ? lane : 0] != 0ull);
-                                // compact t2 into L2 (u16 bit positions) 8 words per round:
-                                // lane h < 16 owns 32-bit half-word h of the round
-                                const u32* t2h = (const u32*)t2s;
-                                unsigned short* L2h = (unsigned short*)L2;
-                                for (u32 h0 = 0; h0 < 2 * Wd; h0 += 16) {
-                                    if (!((nz2 >> (h0 >> 1)) & 0xffu)) continue;
-                                    const u32 hw = h0 + lane;
-                                    u32 m = (lane < 16 && hw < 2 * Wd) ? t2h[hw] : 0u;
-                                    const u32 c = __popc(m);
-                                    const u32 incl = g2m_scan_incl(c);
-                                    const u32 n2 = __shfl_sync(G2M_FULL, incl, 31);
-                                    u32 pos = incl - c;
-                                    while (m) {
-                                        const u32 b = __ffs(m) - 1;
-                                        m &= m - 1;
-                                        L2h[pos++] = (unsigned short)(hw * 32 + b);
-                                    }
-                                    __syncwarp();
+                                for (u32 c2 = 0; c2 < Wd; c2 += CH) {
+                                    if (!((nz2 >> c2) & ((1u << CH) - 1u))) continue;
+                                    const u32 n2 = compact_bits(t2s, c2, min(c2 + CH, Wd), L2);
                                     for (u32 f = lane; f < n2; f += 32) {
-                                        const u32 l = L2h[f];
+                                        const u32 l = L2[f];
                                         const u64* Rl = R + (u64)l * Ws;
                                         u32 mq = nz2 & ~((1u << (l >> 6)) - 1u);   // R_l is zero below word l/64
                                         while (mq) {
@@ -650,18 +690,20 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
 }
 
 // Bucket the sources of this partition by local-graph size class.
-// class 0: d < K-1 (no clique), 1: d <= 64 (warp), 2..5: d <= 128..1024
+// class 0: d < K-1 (no clique), 8: d <= pair_maxd (pairs), 1: d <= 64 (warp), 2..5: d <= 128..1024
 // (CTA, W = 2,4,8,16), 7: 1024 < d <= max_cta_d (CTA, W = 64; k = 3 only),
 // 6: d > max_cta_d (generic kernel). span_max[c]: widest id window of class c.
-__global__ void k_clique_bucket(const u64* off, const u32* nbr, u64 nv, int kmin1, u64 max_cta_d, u64 rr_chunk,
-                                u32 parts, u32 part, u32* lists, u64 list_stride, u64* sizes, u32* span_max) {
+__global__ void k_clique_bucket(const u64* off, const u32* nbr, u64 nv, int kmin1, u64 max_cta_d, u64 pair_maxd,
+                                u64 rr_chunk, u32 parts, u32 part, u32* lists, u64 list_stride, u64* sizes,
+                                u32* span_max) {
     for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x) {
         if (rr_chunk && ((v / rr_chunk) % parts) != part) continue;
         const u64 b = off[v];
         const u64 d = off[v + 1] - b;
         int c;
         if (d < (u64)kmin1 || d == 0) continue;
-        if (d <= 64) c = 1;
+        if (d <= pair_maxd) c = 8;
+        else if (d <= 64) c = 1;
         else if (d <= 128) c = 2;
         else if (d <= 256) c = 3;
         else if (d <= 512) c = 4;

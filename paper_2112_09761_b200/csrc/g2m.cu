@@ -152,6 +152,7 @@ struct DevState {
     int sms = 0;
     uint64_t launches = 0;   // kernels of ours launched on this device (g2m_run_stats.launches)
     DevBuf tmp1, tmp2;       // grow-only scratch of the preprocessing passes (rank relabelling)
+    DevBuf frontier;         // BFS level-3 frontier items (grow-only)
     DevBuf c4slab;           // 4-cycle staging slabs, one per block
 };
 
@@ -1063,7 +1064,8 @@ extern "C" int g2m_run_bfs(const g2m_kernel* ke, const g2m_kernel* kc, const g2m
     uint64_t fbytes = frontier_bytes ? frontier_bytes : (uint64_t)fr / 4;
     fbytes = std::min<uint64_t>(fbytes, (uint64_t)fr / 2);
     const uint64_t cap = std::max<uint64_t>(fbytes / sizeof(G2MItem), 64);
-    DevBuf items, fn;
+    DevBuf& items = st->frontier;   // grow-only, kept across calls
+    DevBuf fn;
     G2M_TRY(items.ensure(cap * sizeof(G2MItem)));
     G2M_TRY(fn.ensure(8));
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
@@ -1248,9 +1250,19 @@ __global__ void k_heavy_fill(const u64* off, const u32* verts, u64 n, const u64*
     }
 }
 
-// Source classes of k_clique_bucket: 1 warp tier, 2..5 CTA tiers W = 2..16,
-// 7 CTA tier W = 64 (k = 3 only: no rows), 6 generic plan kernel.
-static const int kClasses = 8;
+// Source classes of k_clique_bucket: 8 pair tier (d <= 16), 1 warp tier,
+// 2..5 CTA tiers W = 2..16, 7 CTA tier W = 64 (k = 3) / 32 (rows in L2),
+// 6 generic plan kernel.
+static const int kClasses = 9;
+
+// Sources up to this out-degree go to the pair tier (G2M_PAIR_MAXD, 0 = off).
+static u64 pair_maxd() {
+    static const u64 v = [] {
+        const char* e = getenv("G2M_PAIR_MAXD");
+        return e ? std::min<u64>(strtoull(e, nullptr, 10), 16) : (u64)16;
+    }();
+    return v;
+}
 
 template <int K, bool SUP = false>
 static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const u32* lists, u64 stride,
@@ -1273,6 +1285,16 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         if (dbg) fprintf(stderr, "[g2m]   launch %d: %.3f ms\n", slot, ms);
         return G2M_OK;
     };
+    if (kClasses > 8 && sizes[8]) {
+        constexpr int WPB = 8;
+        u64 grab = std::max<u64>(1, std::min<u64>(16, sizes[8] / ((u64)st->sms * 64 * WPB)));
+        G2M_TRY(timed([&] {
+            ++st->launches;
+            k_clique_pairs<K, WPB><<<st->sms * 8, WPB * 32, 0, st->stream>>>(off, nbr, lists + 8 * stride, sizes[8],
+                                                                             next + slot, grab, count);
+        }));
+        ++slot;
+    }
     if (sizes[1]) {
         constexpr int WPB = 8;
         u64 grab = std::max<u64>(1, std::min<u64>(8, sizes[1] / ((u64)st->sms * 64 * WPB)));
@@ -1376,8 +1398,8 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     if (g->nv) {
         ++st->launches;
         g2m_clique::k_clique_bucket<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(
-            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 2048, rr_chunk, parts, pt, st->tasks_b.as<u32>(), stride,
-            dsizes, dspans);
+            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 2048, pair_maxd(), rr_chunk, parts, pt, st->tasks_b.as<u32>(),
+            stride, dsizes, dspans);
         G2M_CUDA(cudaGetLastError());
     }
     uint64_t sizes[kClasses];
@@ -1387,8 +1409,8 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     const u32* lists = st->tasks_b.as<u32>();
     if (getenv("G2M_DEBUG"))
-        fprintf(stderr, "[g2m] clique k=%d buckets: warp<=64:%llu 128:%llu 256:%llu 512:%llu 1024:%llu 4096:%llu generic:%llu\n",
-                k, (unsigned long long)sizes[1], (unsigned long long)sizes[2], (unsigned long long)sizes[3],
+        fprintf(stderr, "[g2m] clique k=%d buckets: pairs %llu warp<=64:%llu 128:%llu 256:%llu 512:%llu 1024:%llu 4096:%llu generic:%llu\n",
+                k, (unsigned long long)sizes[8], (unsigned long long)sizes[1], (unsigned long long)sizes[2], (unsigned long long)sizes[3],
                 (unsigned long long)sizes[4], (unsigned long long)sizes[5], (unsigned long long)sizes[7],
                 (unsigned long long)sizes[6]);
     {
@@ -1507,7 +1529,7 @@ extern "C" int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, 
     if (og->nv) {
         ++st->launches;
         g2m_clique::k_clique_bucket<<<grid_for(st, og->nv, 256), 256, 0, st->stream>>>(
-            off, nbr, og->nv, 2, 4096, 0, 1, 0, st->tasks_b.as<u32>(), stride, dsizes, dspans);
+            off, nbr, og->nv, 2, 4096, 0, 0, 1, 0, st->tasks_b.as<u32>(), stride, dsizes, dspans);
         G2M_CUDA(cudaGetLastError());
     }
     uint64_t sizes[kClasses];

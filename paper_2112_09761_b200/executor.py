@@ -345,6 +345,14 @@ FRONTIER_ITEM = 16              # bytes per item (G2MItem)
 SKEW_FOR_BFS = 8.0              # max degree / average degree that makes DFS lopsided
 
 
+def frontier_estimate(g: Graph, forest: PlanForest, tasks, chunk: int) -> int:
+    """Upper bound (bytes) of the level-3 frontier of the BFS runtime:
+    nodes3 * (Σ_tasks d(v1) / chunk + tasks) items, Σ_tasks d(v1) <= Σ_v d(v)^2."""
+    n3 = codegen.frontier_nodes(forest)
+    items = n3 * (float(g.sum_degree_sq()) / max(chunk, 1) + len(tasks))
+    return int(items * FRONTIER_ITEM)
+
+
 def choose_search(g: Graph, forest: PlanForest, tasks, cfg: ExecutionConfig | None = None,
                   sink=None) -> tuple[str, str]:
     """DFS or bounded-frontier BFS for one forest on one graph, with the
@@ -366,9 +374,7 @@ def choose_search(g: Graph, forest: PlanForest, tasks, cfg: ExecutionConfig | No
         return "dfs", "no level-3 subtree to split (or list/labeled/vertex tasks)"
     if mode == "auto" and kernel_family(g, forest, tasks, sink) != "plan":
         return "dfs", f"{kernel_family(g, forest, tasks, sink)} kernels, not the plan kernel"
-    sq = float(g.sum_degree_sq())
-    items = n3 * (sq / max(cfg.bfs_chunk, 1) + len(tasks))
-    est = int(items * FRONTIER_ITEM)
+    est = frontier_estimate(g, forest, tasks, cfg.bfs_chunk)
     budget = cfg.frontier_bytes or FRONTIER_BUDGET
     if mode == "bfs":
         return "bfs", f"bounded-frontier BFS requested (frontier <= {est} B, blocks of <= {budget} B)"
@@ -447,8 +453,11 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
             words = np.zeros(2 * max(ce.gen.num_patterns, 1), dtype=np.uint64)
             stats = N.RunStats()
             rcfg = run_config if run_config is not None else N.RunConfig()
+            # frontier buffer: the whole estimated frontier when it fits the budget
+            fbytes = min(frontier_estimate(g, forest, tasks, ecfg.bfs_chunk) + (1 << 20),
+                         int(ecfg.frontier_bytes or FRONTIER_BUDGET))
             N.check(N.lib().g2m_run_bfs(ce.handle, cc.handle, dg.handle, C.byref(spec), C.byref(rcfg),
-                                        int(ecfg.bfs_chunk), int(ecfg.frontier_bytes or FRONTIER_BUDGET),
+                                        int(ecfg.bfs_chunk), int(fbytes),
                                         N.ptr(words, C.c_uint64), C.byref(stats)), "bfs")
             del keep
             return _counts_from(words, ce.gen.pattern_ids), stats, False, ce

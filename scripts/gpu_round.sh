@@ -1,4 +1,4 @@
-# full check: GPU test suite, smoke, default bench (all keys), reference arm, other configs
+# full check: GPU test suite, smoke, default bench (all keys), reference arm, other configs, ncu evidence
 mkdir -p gpurun_out
 T=${1:-r01}
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_pytest_gpu.log 2>&1; tail -3 gpurun_out/${T}_pytest_gpu.log
@@ -8,3 +8,8 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/$
 for w in tc cl5 c4 diamond mc3 mc4; do
   timeout 900 python bench.py --workload $w --steps 3 --warmup 3 --cpu-seconds 10 > gpurun_out/${T}_bench_$w.json 2> gpurun_out/${T}_bench_$w.err; echo $w rc=$?; cut -c1-200 gpurun_out/${T}_bench_$w.json
 done
+# ncu: launch list of one cold cl4 step + full capture of its mining kernels
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_cl4_launches.csv \
+  python bench.py --workload cl4 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-roofline > /dev/null 2>&1; echo launches rc=$?
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_clique_(warp|cta)" -c 8 \
+  -o gpurun_out/${T}_cl4_full -f python bench.py --workload cl4 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-roofline > /dev/null 2>&1; echo full rc=$?
