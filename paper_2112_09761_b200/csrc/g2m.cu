@@ -1347,7 +1347,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     using std::integral_constant;
     using F = std::false_type;
     G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 16>{}, F{}, 2, 2));
-    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, F{}, 3, 2));
+    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, F{}, 3, 3));
     G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, F{}, 4, 2));
     G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, F{}, 5, 1));
     if constexpr (K == 3)
