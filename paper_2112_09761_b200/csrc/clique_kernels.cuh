@@ -95,7 +95,7 @@ __device__ __forceinline__ u32 probe_rows(const u64* __restrict__ off, const u32
         ro = __ldg(off + v);
         rn = (u32)(__ldg(off + v + 1) - ro);
         // out-neighbours of v are > v >= A0; drop the tail beyond A_last
-        if (rn > 32 && __ldg(nbr + ro + rn - 1) > hi) rn = g2m_lb(nbr + ro, rn, hi + 1u);
+        if (rn > 64 && __ldg(nbr + ro + rn - 1) > hi) rn = g2m_lb(nbr + ro, rn, hi + 1u);
     }
     const u32 incl = g2m_scan_incl(rn);
     const u32 tot = __shfl_sync(G2M_FULL, incl, 31);
@@ -493,7 +493,7 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                 ro = __ldg(off + y);
                 rn = (u32)(__ldg(off + y + 1) - ro);
                 // out-neighbours of y are > y >= A0; drop the tail beyond A_last
-                if (rn > 32 && __ldg(nbr + ro + rn - 1) > alast) rn = g2m_lb(nbr + ro, rn, alast + 1u);
+                if (rn > 64 && __ldg(nbr + ro + rn - 1) > alast) rn = g2m_lb(nbr + ro, rn, alast + 1u);
             }
             const bool lng = rn >= kLongRow;     // probed row by row, not concatenated
             const u32 lm = __ballot_sync(G2M_FULL, lng);
@@ -567,10 +567,13 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
             }
         if constexpr (K > 3) {
             for (;;) {
-                u32 i = 0;
-                if (lane == 0) i = atomicAdd(&s_cnt, 1u);
-                i = __shfl_sync(G2M_FULL, i, 0);
-                if (i >= d) break;
+                constexpr u32 G = K == 4 ? 4u : 1u;   // rows per grab (k = 5 rows are heavy)
+                u32 ig = 0;
+                if (lane == 0) ig = atomicAdd(&s_cnt, G);
+                ig = __shfl_sync(G2M_FULL, ig, 0);
+                if (ig >= d) break;
+                const u32 ie = min(ig + G, d);
+                for (u32 i = ig; i < ie; ++i) {
                 const u64* Ri = R + (u64)i * Ws;
                 const u64 myw = lane < Wd ? Ri[lane] : 0ull;
                 const u32 nzw = __ballot_sync(G2M_FULL, myw != 0ull);
@@ -677,6 +680,7 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                         }
                     }
                     __syncwarp();
+                }
                 }
             }
         }
