@@ -303,8 +303,8 @@ __device__ __forceinline__ u32 compact_bits(const u64* words, u32 q0, u32 q1, u3
     return n;
 }
 
-// Per-warp scratch of the CTA tier (u32 words): L1[256] L2[256] (k > 3).
-__host__ __device__ constexpr u32 cta_warp_words(int K) { return K > 3 ? 512u : 0u; }
+// Per-warp scratch of the CTA tier (u32 words): L1[256] (k >= 4), L2[256] (k = 5).
+__host__ __device__ constexpr u32 cta_warp_words(int K) { return K > 4 ? 512u : (K == 4 ? 256u : 0u); }
 
 // u64 words of the local-graph rows R and the per-warp row buffers T.
 __host__ __device__ constexpr size_t cta_row_words(int K, int W, int NW) {
