@@ -235,11 +235,20 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    # G2M_BENCH_BACKEND=gloo: CPU collectives and ranks folded onto the visible
+    # GPUs -- exercises the N>1 path on a single-GPU box (timings meaningless)
+    backend = os.environ.get("G2M_BENCH_BACKEND", "nccl")
+    coll_dev = None
     if world > 1:
         import torch
         import torch.distributed as dist
+        if backend == "gloo":
+            local = local % max(torch.cuda.device_count(), 1)
+            coll_dev = "cpu"
+        else:
+            coll_dev = f"cuda:{local}"
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     if args.impl == "reference" and rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -325,9 +334,8 @@ def main():
     my_ms = float(np.mean(dev_ms))
     total_counts = counts
     if dist is not None:   # the job's time is its slowest rank; counts add up exactly
-        dev = f"cuda:{local}"
-        ms = D.allreduce_max(my_ms, device=dev)
-        total_counts = D.allreduce_counts(counts, device=dev)
+        ms = D.allreduce_max(my_ms, device=coll_dev)
+        total_counts = D.allreduce_counts(counts, device=coll_dev)
     else:
         ms = my_ms
     value = E / (ms / 1000.0)
@@ -355,7 +363,7 @@ def main():
                 e2e_s.append(dt)
         e_ms = float(np.mean(e2e_s)) * 1000.0
         if dist is not None:
-            e_ms = D.allreduce_max(e_ms, device=f"cuda:{local}")
+            e_ms = D.allreduce_max(e_ms, device=coll_dev)
         e2e = {"value": E / (e_ms / 1000.0), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(16 * len(counts) + 8 * 32), "ms_per_step": e_ms,
                "path": "public API (pm.k_clique / triangle_count / subgraph_listing / k_motif) on a "
@@ -372,18 +380,24 @@ def main():
         frac = args.balg_sample
         if frac is None and kind == "sl" and WORKLOADS[args.workload][1] == "4-cycle" and E > 10 ** 7:
             frac = 1e-3     # the reference 4-cycle plan is quadratic in hub degree: sample it
-        if frac and world == 1:
-            # seeded uniform task sample through the instrumented plan kernel, scaled up
-            ntask = len(tasks)
-            rng = np.random.default_rng(11)
-            idx = np.sort(rng.choice(ntask, size=max(1, int(ntask * frac)), replace=False))
-            _, bst, _, _ = EX.execute(gd, forest, tasks, device=local, index=idx, instrument=True)
-            balg = int(int(bst.alg_bytes) * ntask / len(idx))
-            balg_how = f"sampled: {len(idx)} of {ntask} tasks (seeded uniform), scaled"
+        if frac:
+            # seeded uniform sample of the whole job's tasks through the
+            # instrumented plan kernel, scaled up (rank 0 only)
+            balg = 0
+            if rank == 0:
+                ntask = len(tasks)
+                rng = np.random.default_rng(11)
+                idx = np.sort(rng.choice(ntask, size=max(1, int(ntask * frac)), replace=False))
+                _, bst, _, _ = EX.execute(gd, forest, tasks, device=local, index=idx, instrument=True)
+                balg = int(int(bst.alg_bytes) * ntask / len(idx))
+                balg_how = f"sampled: {len(idx)} of {ntask} tasks (seeded uniform), scaled"
         else:
             _, bst, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, instrument=True)
             balg = int(bst.alg_bytes)
             balg_how = "exact: instrumented plan kernel over every task"
+        if dist is not None:   # whole job: bytes add up over ranks, time is the slowest rank's
+            balg = D.allreduce_counts({"b": balg}, device=coll_dev)["b"]
+            kms = D.allreduce_max(kms, device=coll_dev)
         log("algorithmic bytes", balg, balg_how, "in", round(time.perf_counter() - t_b, 2), "s")
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"

@@ -714,7 +714,13 @@ __global__ void k_clique_bucket(const u64* off, const u32* nbr, u64 nv, int kmin
         else if (d <= 1024) c = 5;
         else if (d <= max_cta_d) c = 7;
         else c = 6;
-        const u64 slot = atomicAdd(sizes + c, 1ull);
+        // warp-aggregated append: one atomic per (warp, class) instead of per vertex
+        const u32 peers = __match_any_sync(__activemask(), c);
+        const u32 leader = __ffs(peers) - 1;
+        u64 base = 0;
+        if (g2m_lane() == leader) base = atomicAdd(sizes + c, (u64)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        const u64 slot = base + __popc(peers & g2m_lanemask_lt());
         lists[(u64)c * list_stride + slot] = (u32)v;
         if (c >= 2 && c != 6) atomicMax(span_max + c, __ldg(nbr + b + d - 1) - __ldg(nbr + b) + 1u);
     }
