@@ -108,24 +108,29 @@ static double ms_since(Clock::time_point t0) {
 // device buffers
 // ---------------------------------------------------------------------------
 
+// Allocations are stream-ordered (cudaMallocAsync / cudaFreeAsync) on the
+// stream of the device the current API call works on (set by dev_state), from
+// the device's memory pool with no release threshold: graphs created and freed
+// call after call reuse pooled memory instead of cudaMalloc/cudaFree round trips.
+static thread_local cudaStream_t t_alloc_stream = nullptr;
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t s = nullptr;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
+    ~DevBuf() { release(); }
     int ensure(size_t n) {
         if (n <= bytes && p) return G2M_OK;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
+        release();
         if (n == 0) n = 16;
-        cudaError_t e = cudaMalloc(&p, n);
+        s = t_alloc_stream;
+        cudaError_t e = s ? cudaMallocAsync(&p, n, s) : cudaMalloc(&p, n);
         if (e != cudaSuccess) {
             cudaGetLastError();
+            p = nullptr;
             return fail(G2M_ECUDA, std::string("cudaMalloc(") + std::to_string(n) +
                                        "): " + cudaGetErrorString(e));
         }
@@ -133,7 +138,10 @@ struct DevBuf {
         return G2M_OK;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (s) cudaFreeAsync(p, s);
+            else cudaFree(p);
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -172,9 +180,16 @@ static int dev_state(int dev, DevState** out) {
         G2M_CUDA(cudaEventCreate(&st->evs0));
         G2M_CUDA(cudaEventCreate(&st->evs1));
         G2M_CUDA(cudaDeviceGetAttribute(&st->sms, cudaDevAttrMultiProcessorCount, dev));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
         it = g_devs.emplace(dev, std::move(st)).first;
     }
     *out = it->second.get();
+    t_alloc_stream = (*out)->stream;
     return G2M_OK;
 }
 
@@ -1520,7 +1535,7 @@ extern "C" int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, 
     G2M_TRY(st->counters.ensure(32 * 8));
     u64* ctr = st->counters.as<u64>();
     G2M_CUDA(cudaMemsetAsync(ctr, 0, 32 * 8, st->stream));
-    DevBuf tsup;
+    DevBuf& tsup = st->tmp1;   // grow-only scratch (the rank build that also uses it is done)
     G2M_TRY(tsup.ensure(std::max<u64>(og->slots, 1) * 4));
     G2M_CUDA(cudaMemsetAsync(tsup.p, 0, std::max<u64>(og->slots, 1) * 4, st->stream));
     const u64 stride = std::max<u64>(og->nv, 1);
