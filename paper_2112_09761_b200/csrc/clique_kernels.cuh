@@ -428,7 +428,7 @@ __device__ __forceinline__ u32 cta_probe(const u64* __restrict__ off, const u32*
 template <int K, int W, int NW, bool GR = false, bool SUP = false>
 __global__ void __launch_bounds__(NW * 32)
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows, u32* tsup) {
+             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows, u32* tsup, u32 split) {
     constexpr u32 CH = 4;             // words compacted per round (<= 256 candidates)
     extern __shared__ __align__(16) u64 smem[];
     // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64   (K > 3 only)
@@ -466,7 +466,10 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
             s_flat = 0;
         }
         __syncthreads();
-        const u64 t = s_u;
+        // work item s_u = (source, part): with split > 1 every part builds the
+        // source's local graph and counts the rows i = part (mod split)
+        const u64 t = s_u / split;
+        const u32 part = (u32)(s_u % split);
         if (t >= nverts) break;
         const u32 u = __ldg(verts + t);
         const u64 b = __ldg(off + u);
@@ -571,39 +574,59 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                 u32 ig = 0;
                 if (lane == 0) ig = atomicAdd(&s_cnt, G);
                 ig = __shfl_sync(G2M_FULL, ig, 0);
-                if (ig >= d) break;
-                const u32 ie = min(ig + G, d);
-                for (u32 i = ig; i < ie; ++i) {
+                const u32 nmine = (d - part + split - 1) / split;   // rows part, part+split, ...
+                if (ig >= nmine) break;
+                const u32 ie = min(ig + G, nmine);
+                for (u32 ii = ig; ii < ie; ++ii) {
+                const u32 i = part + ii * split;
                 const u64* Ri = R + (u64)i * Ws;
                 const u64 myw = lane < Wd ? Ri[lane] : 0ull;
                 const u32 nzw = __ballot_sync(G2M_FULL, myw != 0ull);
                 if (!nzw) continue;
                 if constexpr (K == 5) {
                     // 4-cliques with local source i = triangles of the sub-DAG on
-                    // R_i. With n1 = |R_i| <= 64 its rows are single words:
-                    // S_k bit m <=> L1[m] in R_{L1[k]}, one ballot pair per k.
+                    // R_i. With n1 = |R_i| <= 128 its rows fit two words:
+                    // S_k bit m <=> L1[m] in R_{L1[k]}, four ballots per k.
                     const u32 n1 = __reduce_add_sync(G2M_FULL, (u32)__popcll(myw));
-                    if (n1 <= 64) {
+                    if (n1 <= 128) {
+                        // sub-DAG rows of up to 128 bits (two words): lane q*32+l holds
+                        // candidate c[q]; S_k = ballots of "c in R_{L1[k]}"
                         compact_bits(Ri, 0, Wd, L1);
-                        u64* SS = (u64*)L2;
-                        const u32 c0 = lane < n1 ? L1[lane] : 0u;
-                        const u32 c1 = lane + 32 < n1 ? L1[lane + 32] : 0u;
+                        u32 c[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) c[q] = lane + 32u * q < n1 ? L1[lane + 32 * q] : 0u;
+                        __syncwarp();
+                        u64* SS = (u64*)L1;          // [n1][2] u64, over L1 and L2
                         for (u32 k = 0; k < n1; ++k) {
-                            const u64* Rk = R + (u64)L1[k] * Ws;   // no bits at or below L1[k]
-                            const bool b0 = lane < n1 && ((Rk[c0 >> 6] >> (c0 & 63u)) & 1ull);
-                            const bool b1 = lane + 32 < n1 && ((Rk[c1 >> 6] >> (c1 & 63u)) & 1ull);
-                            const u32 s0 = __ballot_sync(G2M_FULL, b0);
-                            const u32 s1 = __ballot_sync(G2M_FULL, b1);
-                            if (lane == 0) SS[k] = ((u64)s1 << 32) | s0;
+                            const u32 qk = k >> 5;
+                            const u32 src = qk == 0 ? c[0] : (qk == 1 ? c[1] : (qk == 2 ? c[2] : c[3]));
+                            const u64* Rk = R + (u64)__shfl_sync(G2M_FULL, src, k & 31u) * Ws;
+                            u32 sw[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const bool bq = lane + 32u * q < n1 && (u32)q >= qk &&
+                                                ((Rk[c[q] >> 6] >> (c[q] & 63u)) & 1ull);
+                                sw[q] = __ballot_sync(G2M_FULL, bq);
+                            }
+                            if (lane == 0) {
+                                SS[2 * k] = ((u64)sw[1] << 32) | sw[0];
+                                SS[2 * k + 1] = ((u64)sw[3] << 32) | sw[2];
+                            }
                         }
                         __syncwarp();
                         for (u32 k = lane; k < n1; k += 32) {
-                            const u64 Sk = SS[k];
-                            u64 it = Sk;
+                            const u64 S0 = SS[2 * k], S1 = SS[2 * k + 1];
+                            u64 it = S0;
                             while (it) {
                                 const int l = __ffsll(it) - 1;
                                 it &= it - 1;
-                                acc += (u64)__popcll(Sk & SS[l]);
+                                acc += (u64)__popcll(S0 & SS[2 * l]) + (u64)__popcll(S1 & SS[2 * l + 1]);
+                            }
+                            it = S1;
+                            while (it) {
+                                const int l = 64 + __ffsll(it) - 1;
+                                it &= it - 1;
+                                acc += (u64)__popcll(S1 & SS[2 * l + 1]);
                             }
                         }
                         __syncwarp();

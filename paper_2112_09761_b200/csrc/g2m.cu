@@ -1342,7 +1342,11 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
         G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem));
-        const u64 grid = std::min<u64>(sizes[cls], (u64)st->sms * std::max(occ, 1));
+        // a handful of huge sources (the L2-row tier) would leave most SMs idle:
+        // split their counting over several blocks each (k > 3)
+        const u32 split = (GR && K > 3) ? (u32)std::max<u64>(1, std::min<u64>(32, (u64)st->sms / sizes[cls])) : 1u;
+        const u64 items = sizes[cls] * split;
+        const u64 grid = std::min<u64>(items, (u64)st->sms * std::max(occ, 1));
         u64* grows = nullptr;
         if (GR) {
             G2M_TRY(slab.ensure(grid * cta_row_words(K, W, NW) * 8));
@@ -1354,7 +1358,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         G2M_TRY(timed([&] {
             ++st->launches;
             kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
-                                                                 next + slot, count, bmw, grows, tsup);
+                                                                 next + slot, count, bmw, grows, tsup, split);
         }));
         ++slot;
         return G2M_OK;
