@@ -306,6 +306,13 @@ __device__ __forceinline__ u32 compact_bits(const u64* words, u32 q0, u32 q1, u3
 // Per-warp scratch of the CTA tier (u32 words): L1[256] (k >= 4), L2[256] (k = 5).
 __host__ __device__ constexpr u32 cta_warp_words(int K) { return K > 4 ? 512u : (K == 4 ? 256u : 0u); }
 
+// The fallback hash map (keys + vals, 256W words) is only live while rows are
+// probed, the per-warp candidate lists only while they are counted: they
+// share one region.
+__host__ __device__ constexpr size_t cta_union_words(int K, int W, int NW) {
+    return (size_t)256 * W > (size_t)NW * cta_warp_words(K) ? (size_t)256 * W : (size_t)NW * cta_warp_words(K);
+}
+
 // u64 words of the local-graph rows R and the per-warp row buffers T.
 __host__ __device__ constexpr size_t cta_row_words(int K, int W, int NW) {
     return K > 3 ? (size_t)(64 * W + NW) * (W + 1) : 0;
@@ -319,8 +326,7 @@ __host__ __device__ constexpr size_t cta_smem_bytes(int K, int W, int NW, u32 bm
            + (SUP ? (size_t)4 * 2 * 64 * W : 0)                  // support row / column counters
            + (size_t)8 * 64 * W                                  // RB
            + (size_t)4 * 64 * W * 3 + (size_t)4 * 2 * W          // A, RE, LR, BT
-           + (size_t)4 * 256 * W                                 // hash keys + vals
-           + (size_t)NW * 4 * cta_warp_words(K)                  // per-warp scratch
+           + (size_t)4 * cta_union_words(K, W, NW)               // hash (probe) | per-warp scratch (count)
            + (size_t)4 * bmw + (size_t)2 * ((bmw + 1) & ~1u);    // bitmap, pre
 }
 
@@ -441,10 +447,10 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
     u32* RE = A + 64 * W;
     u32* LR = RE + 64 * W;
     u32* BT = LR + 64 * W;
-    u32* HK = BT + 2 * W;
+    u32* HK = BT + 2 * W;             // probe phase
     u32* HV = HK + 128 * W;
-    u32* scr = HV + 128 * W;
-    u32* BM = scr + NW * cta_warp_words(K);
+    u32* scr = HK;                    // count phase (same region, after the barrier)
+    u32* BM = HK + cta_union_words(K, W, NW);
     u16* PRE = (u16*)(BM + bmw);
     u32* SROW = (u32*)(PRE + ((bmw + 1) & ~1u));     // SUP only: [64W] row, [64W] column counters
     u32* SCOL = SROW + 64 * W;

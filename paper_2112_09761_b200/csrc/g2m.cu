@@ -1368,8 +1368,12 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 16>{}, F{}, 2, 2));
     G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, F{}, 3, 3));
     G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, F{}, 4, 2));
-    if constexpr (K == 4)   // one 1024-thread block per SM (the 139 KB of rows allow no second block)
+    // one block per SM (the 139 KB of rows allow no second): as many warps as the
+    // per-warp candidate lists leave room for
+    if constexpr (K == 4)
         G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 32>{}, F{}, 5, 1));
+    else if constexpr (K == 5)
+        G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 24>{}, F{}, 5, 1));
     else
         G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, F{}, 5, 1));
     if constexpr (K == 3)
