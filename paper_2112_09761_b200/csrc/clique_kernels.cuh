@@ -231,7 +231,7 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
 }
 
 // ---------------------------------------------------------------------------
-// pair tier: d <= 16, one warp per source; the local edges a -> b (a, b in A)
+// pair tier: d <= 32, one warp per source; the local edges a -> b (a, b in A)
 // are found by testing every pair of A directly, b in N+(a) by binary search
 // -- d(d-1)/2 lane-parallel tests instead of streaming the out-lists of A,
 // which for small sources are mostly far longer than A itself.
@@ -240,8 +240,8 @@ template <int K, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
 k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
                u64 nverts, u64* next, u64 grab, u64* count) {
-    __shared__ u32 sA[WPB][16];
-    __shared__ __align__(8) u64 sR[WPB][16];
+    __shared__ u32 sA[WPB][32];
+    __shared__ __align__(8) u64 sR[WPB][32];
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
     u32* A = sA[w];
@@ -257,10 +257,8 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
             const u32 u = __ldg(verts + t);
             const u64 b = __ldg(off + u);
             const u32 d = (u32)(__ldg(off + u + 1) - b);
-            if (lane < 16) {
-                A[lane] = lane < d ? __ldg(nbr + b + lane) : 0u;
-                R[lane] = 0;
-            }
+            A[lane] = lane < d ? __ldg(nbr + b + lane) : 0u;
+            R[lane] = 0;
             __syncwarp();
             const u32 np = d * (d - 1) / 2;
             for (u32 p = lane; p < np; p += 32) {

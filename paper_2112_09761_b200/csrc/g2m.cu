@@ -1274,7 +1274,7 @@ static const int kClasses = 9;
 static u64 pair_maxd() {
     static const u64 v = [] {
         const char* e = getenv("G2M_PAIR_MAXD");
-        return e ? std::min<u64>(strtoull(e, nullptr, 10), 16) : (u64)16;
+        return e ? std::min<u64>(strtoull(e, nullptr, 10), 32) : (u64)16;
     }();
     return v;
 }
