@@ -231,7 +231,7 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
 }
 
 // ---------------------------------------------------------------------------
-// pair tier: d <= 32, one warp per source; the local edges a -> b (a, b in A)
+// pair tier: d <= 64, one warp per source; the local edges a -> b (a, b in A)
 // are found by testing every pair of A directly, b in N+(a) by binary search
 // -- d(d-1)/2 lane-parallel tests instead of streaming the out-lists of A,
 // which for small sources are mostly far longer than A itself.
@@ -240,8 +240,8 @@ template <int K, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
 k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
                u64 nverts, u64* next, u64 grab, u64* count) {
-    __shared__ u32 sA[WPB][32];
-    __shared__ __align__(8) u64 sR[WPB][32];
+    __shared__ u32 sA[WPB][64];
+    __shared__ __align__(8) u64 sR[WPB][64];
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
     u32* A = sA[w];
@@ -258,13 +258,18 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
             const u64 b = __ldg(off + u);
             const u32 d = (u32)(__ldg(off + u + 1) - b);
             A[lane] = lane < d ? __ldg(nbr + b + lane) : 0u;
+            A[lane + 32] = lane + 32 < d ? __ldg(nbr + b + lane + 32) : 0u;
             R[lane] = 0;
+            R[lane + 32] = 0;
             __syncwarp();
             const u32 np = d * (d - 1) / 2;
+            const float D = 2.f * (float)d - 1.f;
             for (u32 p = lane; p < np; p += 32) {
-                u32 i = 0, rem = p;
-                while (rem >= d - 1 - i) { rem -= d - 1 - i; ++i; }
-                const u32 j = i + 1 + rem;
+                // row i of pair p in the row-major upper triangle: closed form + fix-up
+                u32 i = (u32)((D - sqrtf(D * D - 8.f * (float)p)) * 0.5f);
+                while (i > 0 && i * (2 * d - i - 1) / 2 > p) --i;
+                while ((i + 1) * (2 * d - i - 2) / 2 <= p) ++i;
+                const u32 j = i + 1 + (p - i * (2 * d - i - 1) / 2);
                 const u32 a = A[i];
                 const u64 ao = __ldg(off + a);
                 if (g2m_has_g(nbr + ao, (u32)(__ldg(off + a + 1) - ao), A[j])) {
@@ -275,6 +280,7 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
             if constexpr (K > 3) {
                 __syncwarp();
                 if (lane < d) acc += Chain1<K - 2>::run(R, R[lane]);
+                if (lane + 32 < d) acc += Chain1<K - 2>::run(R, R[lane + 32]);
             }
             __syncwarp();
         }

@@ -1265,7 +1265,7 @@ __global__ void k_heavy_fill(const u64* off, const u32* verts, u64 n, const u64*
     }
 }
 
-// Source classes of k_clique_bucket: 8 pair tier (d <= 16), 1 warp tier,
+// Source classes of k_clique_bucket: 8 pair tier (d <= 64 by default), 1 warp tier,
 // 2..5 CTA tiers W = 2..16, 7 CTA tier W = 64 (k = 3) / 32 (rows in L2),
 // 6 generic plan kernel.
 static const int kClasses = 9;
@@ -1274,7 +1274,7 @@ static const int kClasses = 9;
 static u64 pair_maxd() {
     static const u64 v = [] {
         const char* e = getenv("G2M_PAIR_MAXD");
-        return e ? std::min<u64>(strtoull(e, nullptr, 10), 32) : (u64)16;
+        return e ? std::min<u64>(strtoull(e, nullptr, 10), 64) : (u64)64;
     }();
     return v;
 }
