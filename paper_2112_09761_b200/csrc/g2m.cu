@@ -1633,7 +1633,7 @@ extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, c
     const u32 nbmax = (u32)((nv >> g2m_c4::kBucketBits) + 2 + 3) & ~3u;   // keeps the u64 scratch aligned
     const size_t stage_smem = g2m_c4::stage_smem_bytes(NW, nbmax);
     const bool tier3 = stage_smem <= (size_t)max_smem;
-    u64 stage_cap = tier3 ? ((u64)8 << 20) : 0;            // wedges per v1 staged (32 MB per block)
+    u64 stage_cap = tier3 ? ((u64)16 << 20) : 0;           // wedges per v1 staged (64 MB per block)
     if (const char* e = getenv("G2M_C4_STAGE_CAP")) stage_cap = std::min<u64>(stage_cap, strtoull(e, nullptr, 10));
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
     G2M_TRY(st->counters.ensure(32 * 8));
