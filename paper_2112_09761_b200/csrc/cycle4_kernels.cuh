@@ -259,7 +259,7 @@ k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* 
 // ---- tier 4: the whole grid on one v1, shared dense counters -----------------
 // The v1's wedges are flattened over the grid: k_c4_rows writes each row's
 // wedge count and first nbr index, a scan makes the ends, and k_c4_grid's
-// warps take 256-element steps (owner row by binary search over the ends),
+// warps take 1024-element steps (owner row by binary search over the ends),
 // so a few huge rows do not serialise the grid.
 __global__ void k_c4_rows(const u64* __restrict__ off, const u32* __restrict__ nbr, u32 r1, u32 l1, u32 lo_x,
                           u64* rn_out, u64* rb_out) {
@@ -275,6 +275,12 @@ __global__ void k_c4_rows(const u64* __restrict__ off, const u32* __restrict__ n
     }
 }
 
+// rb[i] -= start of row i in the flattening, so element e of row i is nbr[rb[i] + e]
+__global__ void k_c4_base(u32 l1, const u64* __restrict__ rn, u64* rb, const u64* __restrict__ re) {
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < l1; i += gridDim.x * blockDim.x)
+        rb[i] -= re[i] - rn[i];
+}
+
 __global__ void __launch_bounds__(512)
 k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const u64* __restrict__ rb,
           const u64* __restrict__ re, u64* ctr, u32* dense, u64* count) {
@@ -283,7 +289,7 @@ k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const
     u64 acc = 0;
     for (;;) {
         u64 e0 = 0;
-        if (lane == 0) e0 = atomicAdd(ctr, 256ull);
+        if (lane == 0) e0 = atomicAdd(ctr, 1024ull);
         e0 = __shfl_sync(G2M_FULL, e0, 0);
         if (e0 >= tot) break;
         // owner of e0: first row with end > e0
@@ -293,14 +299,12 @@ k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const
             if (__ldg(re + lo + h) <= e0) { lo += h + 1; n -= h + 1; } else n = h;
         }
         u32 ow = lo;
-#pragma unroll 2
-        for (u32 k = 0; k < 256; k += 32) {
+#pragma unroll 4
+        for (u32 k = 0; k < 1024; k += 32) {
             const u64 e = e0 + k + lane;
             if (e < tot) {
                 while (__ldg(re + ow) <= e) ++ow;
-                const u64 start = __ldg(re + ow) - __ldg(rn + ow);
-                const u32 x = __ldg(nbr + __ldg(rb + ow) + (e - start));
-                acc += atomicAdd(dense + x, 1u);
+                acc += atomicAdd(dense + __ldg(nbr + __ldg(rb + ow) + e), 1u);
             }
         }
     }

@@ -1760,6 +1760,8 @@ extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, c
                 g2m_c4::k_c4_rows<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(off, nbr, r1, l1, lo_x, rn, rb);
                 size_t t2 = tb;
                 cub::DeviceScan::InclusiveSum(st->cub_tmp.p, t2, rn, re, (int64_t)l1, st->stream);
+                ++st->launches;
+                g2m_c4::k_c4_base<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(l1, rn, rb, re);
                 cudaMemsetAsync(gctr, 0, 8, st->stream);
                 ++st->launches;
                 g2m_c4::k_c4_grid<<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rn, rb, re, gctr, dense, count);
