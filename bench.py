@@ -121,6 +121,12 @@ def make_graph(spec, device: int, pinned: bool, host: bool = False):
     from paper_2112_09761_b200 import graph as GR
     t0 = time.perf_counter()
     kind, size = spec
+    if kind == "rmat" and size >= 25 and not host:
+        # too large for the host generator: R-MAT generated on the device
+        # (same process, device RNG); no host copy (no e2e at this scale)
+        g = GR.rmat_device(size, 16, 1, device=device)
+        return g, None, None, {"gen_s": 0.0, "build_s": round(time.perf_counter() - t0, 2),
+                               "generator": "device R-MAT (counter-based RNG)"}
     if kind == "rmat":
         edges, nv = G.rmat_edges(size, 16, 1), 1 << size
     else:
@@ -272,7 +278,8 @@ def main():
     pj = prepare(args.workload, g)
     gd, forest, tasks = pj.graph, pj.forest, pj.tasks
     build_info["prepare_s"] = round(time.perf_counter() - t_prep, 2)   # incl. device orientation
-    gname = (f"RMAT-{spec[1]} (ef16, Graph500 a=.57 b=c=.19, seed 1)" if spec[0] == "rmat"
+    gname = (f"RMAT-{spec[1]} (ef16, Graph500 a=.57 b=c=.19, seed 1"
+             + (", device RNG)" if build_info.get("generator") else ")") if spec[0] == "rmat"
              else f"power-law n={spec[1]} m=4 seed 3 (cli.gen_synthetic)")
     config = {"workload": f"{desc} on {gname}", "patterns": list(forest.pattern_ids),
               "graph": f"{spec[0]}{spec[1]}", "num_vertices": g.num_vertices,
@@ -343,7 +350,7 @@ def main():
     # e2e through the public API from pinned host buffers (N=1), or the
     # upload/orient/run chain per rank (N>1)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and off_h is not None:
         h2d = off_h.nbytes + nbr_h.nbytes
         e2e_s = []
         nw = max(1, args.warmup // 2)

@@ -164,6 +164,13 @@ int g2m_graph_create(int32_t device, const uint64_t* row_offsets, uint64_t num_v
 int g2m_graph_from_edges(int32_t device, const int64_t* edges, uint64_t num_pairs,
                          uint64_t num_vertices, const uint32_t* labels_or_null,
                          g2m_graph** out);
+/* R-MAT graph built on the device (SURVEY A.6 process: per edge and bit one
+ * uniform draw picks the quadrant with probabilities a, b, c, 1-a-b-c; then
+ * from_edges semantics). The uniforms come from a counter-based hash of
+ * (seed, edge, bit), not numpy's stream: for graphs too large for a host
+ * generator (scale >= 25, BASELINE config C5). */
+int g2m_graph_rmat(int32_t device, int32_t scale, int32_t edgefactor, uint64_t seed, double a, double b,
+                   double c, g2m_graph** out);
 int g2m_graph_orient(const g2m_graph* g, g2m_graph** out);
 int g2m_graph_replicate(const g2m_graph* g, int32_t device, g2m_graph** out);
 int g2m_graph_info_get(const g2m_graph* g, g2m_graph_info* info);

@@ -82,6 +82,8 @@ SIGNATURES = {
                                    C.c_int32, C.POINTER(_P)]),
     "g2m_graph_from_edges": (C.c_int, [C.c_int32, _i64p, C.c_uint64, C.c_uint64, _u32p,
                                        C.POINTER(_P)]),
+    "g2m_graph_rmat": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double,
+                                 C.c_double, C.POINTER(_P)]),
     "g2m_graph_orient": (C.c_int, [_P, C.POINTER(_P)]),
     "g2m_graph_replicate": (C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
     "g2m_graph_info_get": (C.c_int, [_P, C.POINTER(GraphInfo)]),

@@ -51,6 +51,31 @@ struct BitmapProbe {          // direct-address window [base, base + span)
     }
 };
 
+// Two-level window (windows wider than the direct bitmap): one top bit per
+// 64-id block, a rank prefix per top word, and one 64-bit member word plus
+// first local id for each occupied block -- O(span/64 + d) shared words.
+struct TwoLevelProbe {
+    const u32* top;           // [ntop] block-occupancy bits
+    const u32* tpre;          // [ntop] occupied blocks before each top word
+    const u64* blk;           // [occupied] member bits of each occupied block
+    const u16* bpre;          // [occupied] local id of each block's first member
+    u32 base, span;
+    __device__ __forceinline__ u32 get(u32 x) const {
+        const u32 o = x - base;
+        if (o >= span) return G2M_EMPTY;
+        const u32 t = o >> 6;
+        const u32 tw = top[t >> 5];
+        const u32 tb = 1u << (t & 31u);
+        if (!(tw & tb)) return G2M_EMPTY;
+        const u32 r = tpre[t >> 5] + (u32)__popc(tw & (tb - 1u));
+        const u64 w = blk[r];
+        const u64 b = 1ull << (o & 63u);
+        if (!(w & b)) return G2M_EMPTY;
+        return (u32)bpre[r] + (u32)__popcll(w & (b - 1ull));
+    }
+    __device__ __forceinline__ bool has(u32 x) const { return get(x) != G2M_EMPTY; }
+};
+
 struct HashProbe {            // linear probing, load <= 1/2
     const u32* hk;
     const u32* hv;
@@ -438,7 +463,7 @@ __device__ __forceinline__ u32 cta_probe(const u64* __restrict__ off, const u32*
 template <int K, int W, int NW, bool GR = false, bool SUP = false>
 __global__ void __launch_bounds__(NW * 32)
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows, u32* tsup, u32 split) {
+             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows, u32* tsup, u32 split, u32 direct_max) {
     constexpr u32 CH = 4;             // words compacted per round (<= 256 candidates)
     extern __shared__ __align__(16) u64 smem[];
     // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64   (K > 3 only)
@@ -488,7 +513,15 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         const u32 Ws = Wd | 1u;          // odd row stride (bank spread)
         const u32 a0 = __ldg(nbr + b), alast = __ldg(nbr + b + d - 1);
         const u32 span = alast - a0 + 1u;
-        const bool use_bm = span <= bmw * 32u;
+        const bool use_bm = span <= bmw * 32u && span <= direct_max;
+        // two-level window inside the (idle) bitmap region: top [ntop] | tpre [ntop] |
+        // blk [d] u64 | bpre [d] u16
+        const u32 ntop = ((((span + 63u) >> 6) + 31u) >> 5) + 1u & ~1u;
+        const bool use_tl = !use_bm && 2u * ntop + 2u * d + (d + 1u) / 2u + 2u <= bmw;
+        u32* TT = BM;
+        u32* TP = BM + ntop;
+        u64* TB = (u64*)(BM + 2 * ntop);
+        u16* TBP = (u16*)(TB + d);
         // A, window bits, and per-32-row batches of the flattened out-lists
         for (u32 bt = w; bt * 32 < d; bt += NW) {
             const u32 i = bt * 32 + lane;
@@ -502,6 +535,9 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                     atomicOr(BM + (o >> 5), 1u << (o & 31u));
                     // first member of its word: local id base of that word
                     if (i == 0 || ((__ldg(nbr + b + i - 1) - a0) >> 5) != (o >> 5)) PRE[o >> 5] = (u16)i;
+                } else if (use_tl) {
+                    const u32 t = (y - a0) >> 6;
+                    atomicOr(TT + (t >> 5), 1u << (t & 31u));
                 }
                 ro = __ldg(off + y);
                 rn = (u32)(__ldg(off + y + 1) - ro);
@@ -530,7 +566,27 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
             for (u32 x = threadIdx.x; x < d; x += NW * 32) SROW[x] = SCOL[x] = 0;
         __syncthreads();
         u32 hl = 0;
-        if (!use_bm) {
+        if (use_tl) {
+            // rank prefix of the top words (warp 0 scans, 32 words per step), then
+            // each member sets its bit in its block's word
+            if (w == 0) {
+                u32 carry = 0;
+                for (u32 q0 = 0; q0 < ntop; q0 += 32) {
+                    const u32 q = q0 + lane;
+                    const u32 c = q < ntop ? (u32)__popc(TT[q]) : 0u;
+                    const u32 incl = g2m_scan_incl(c);
+                    if (q < ntop) TP[q] = carry + incl - c;
+                    carry += __shfl_sync(G2M_FULL, incl, 31);
+                }
+            }
+            __syncthreads();
+            for (u32 x = threadIdx.x; x < d; x += NW * 32) {
+                const u32 o = A[x] - a0, t = o >> 6;
+                const u32 r = TP[t >> 5] + (u32)__popc(TT[t >> 5] & ((1u << (t & 31u)) - 1u));
+                atomicOr((u32*)(TB + r) + ((o >> 5) & 1u), 1u << (o & 31u));
+                if (x == 0 || ((A[x - 1] - a0) >> 6) != t) TBP[r] = (u16)x;
+            }
+        } else if (!use_bm) {
             hl = g2m_hlog(d);
             g2m_hmap_build(HK, HV, hl, A, d, threadIdx.x, NW * 32);
         }
@@ -568,6 +624,9 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         if (use_bm)
             hits = cta_probe<K, NW, SUP>(off, nbr, A, RE, RB, LR, nlong, alast, d, tot, &s_lrow, &s_flat, R, Ws,
                                          BitmapProbe{BM, PRE, a0, span}, S);
+        else if (use_tl)
+            hits = cta_probe<K, NW, SUP>(off, nbr, A, RE, RB, LR, nlong, alast, d, tot, &s_lrow, &s_flat, R, Ws,
+                                         TwoLevelProbe{TT, TP, TB, TBP, a0, span}, S);
         else
             hits = cta_probe<K, NW, SUP>(off, nbr, A, RE, RB, LR, nlong, alast, d, tot, &s_lrow, &s_flat, R, Ws,
                                          HashProbe{HK, HV, hl, a0, alast}, S);
@@ -720,6 +779,8 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         // clear the window bits of this source (the bitmap stays all-zero between sources)
         if (use_bm)
             for (u32 x = threadIdx.x; x < d; x += NW * 32) BM[(A[x] - a0) >> 5] = 0;
+        else if (use_tl)   // everything the two-level window wrote
+            for (u32 x = threadIdx.x; x < 2u * ntop + 2u * d + (d + 1u) / 2u + 2u; x += NW * 32) BM[x] = 0;
         __syncthreads();
     }
     acc = g2m_wsum(acc);

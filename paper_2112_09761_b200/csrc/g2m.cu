@@ -477,14 +477,58 @@ extern "C" int g2m_graph_replicate(const g2m_graph* g, int32_t device, g2m_graph
 
 // ---- CSR construction on the device (graph.py:116-142)
 
+// Both directions of every non-loop edge as keys u*n+v (warp-aggregated appends).
+__device__ __forceinline__ void emit_pair_keys(u64 u, u64 v, bool ok, u64 n, u64* keys, u64* nkeys) {
+    const u32 m = __ballot_sync(__activemask(), ok);
+    if (!m) return;
+    const u32 lane = g2m_lane();
+    const u32 leader = __ffs(m) - 1;
+    u64 base = 0;
+    if (lane == leader) base = atomicAdd(nkeys, 2ull * __popc(m));
+    base = __shfl_sync(__activemask(), base, leader);
+    if (ok) {
+        const u64 slot = base + 2ull * __popc(m & g2m_lanemask_lt());
+        keys[slot] = u * n + v;
+        keys[slot + 1] = v * n + u;
+    }
+}
+
 __global__ void k_edge_keys(const i64* edges, u64 m, u64 n, u64* keys, u64* nkeys) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
-        u64 u = (u64)edges[2 * i], v = (u64)edges[2 * i + 1];
-        if (u != v) {
-            u64 slot = atomicAdd(nkeys, 2ull);
-            keys[slot] = u * n + v;
-            keys[slot + 1] = v * n + u;
-        }
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    const u64 m32 = (m + 31) & ~(u64)31;   // whole warps iterate together
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m32; i += stride) {
+        u64 u = 0, v = 0;
+        if (i < m) { u = (u64)edges[2 * i]; v = (u64)edges[2 * i + 1]; }
+        emit_pair_keys(u, v, i < m && u != v, n, keys, nkeys);
+    }
+}
+
+// R-MAT edges (Graph500 quadrant probabilities a, b, c, d = 1-a-b-c), one
+// counter-based uniform per (edge, bit): the same process as SURVEY A.6 with
+// a device RNG instead of numpy's stream (graphs of scale >= 25 do not fit a
+// host-side generator).
+__device__ __forceinline__ double rmat_uniform(u64 seed, u64 i, u32 bit) {
+    u64 z = seed * 0x9E3779B97F4A7C15ull + i * 0xD1B54A32D192ED03ull + (u64)bit * 0xABC98388FB8FAC03ull;
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27; z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+__global__ void k_rmat_keys(u64 m, int scale, u64 seed, double a, double b, double c, u64 n, u64* keys,
+                            u64* nkeys) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    const u64 m32 = (m + 31) & ~(u64)31;
+    const double ab = a + b, abc = a + b + c;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m32; i += stride) {
+        u64 u = 0, v = 0;
+        if (i < m)
+            for (int bit = 0; bit < scale; ++bit) {
+                const double r = rmat_uniform(seed, i, bit);
+                u |= (u64)(r >= ab) << bit;
+                v |= (u64)((r >= a && r < ab) || r >= abc) << bit;
+            }
+        emit_pair_keys(u, v, i < m && u != v, n, keys, nkeys);
     }
 }
 
@@ -497,55 +541,44 @@ __global__ void k_keys_to_csr(const u64* keys, u64 nk, u64 n, u32* nbr, u64* cnt
     }
 }
 
-extern "C" int g2m_graph_from_edges(int32_t device, const int64_t* edges, uint64_t m,
-                                    uint64_t num_vertices, const uint32_t* labels, g2m_graph** out) {
-    if (!out) return fail(G2M_EUSAGE, "null output handle");
-    if (2 * m > (uint64_t)INT32_MAX) return fail(G2M_EUSAGE, "edge list too large for one device sort");
-    DevState* st;
-    G2M_TRY(dev_state(device, &st));
-    std::lock_guard<std::mutex> lk(st->mu);
-    G2M_CUDA(cudaSetDevice(device));
-    const uint64_t n = num_vertices;
-    DevBuf din, keys, keys2, nk, cnt;
-    G2M_TRY(din.ensure(std::max<uint64_t>(m, 1) * 16));
-    G2M_TRY(keys.ensure(std::max<uint64_t>(2 * m, 1) * 8));
-    G2M_TRY(keys2.ensure(std::max<uint64_t>(2 * m, 1) * 8));
-    G2M_TRY(nk.ensure(16));
-    G2M_TRY(cnt.ensure(std::max<uint64_t>(n, 1) * 8));
-    G2M_CUDA(cudaMemsetAsync(nk.p, 0, 16, st->stream));
-    G2M_CUDA(cudaMemsetAsync(cnt.p, 0, std::max<uint64_t>(n, 1) * 8, st->stream));
-    if (m) {
-        G2M_CUDA(cudaMemcpyAsync(din.p, edges, m * 16, cudaMemcpyHostToDevice, st->stream));
-        k_edge_keys<<<grid_for(st, m, 256), 256, 0, st->stream>>>(din.as<i64>(), m, n, keys.as<u64>(), nk.as<u64>());
-        G2M_CUDA(cudaGetLastError());
-    }
-    uint64_t nkeys = 0;
-    G2M_CUDA(cudaMemcpyAsync(&nkeys, nk.p, 8, cudaMemcpyDeviceToHost, st->stream));
-    G2M_CUDA(cudaStreamSynchronize(st->stream));
+// Sorted, deduplicated keys -> CSR graph (graph.py:116-142: symmetric, no
+// self loops, no duplicates, rows ascending).
+static int keys_to_graph(DevState* st, int device, uint64_t n, DevBuf& keys, DevBuf& keys2, DevBuf& nk,
+                         uint64_t nkeys, const uint32_t* labels, g2m_graph** out) {
     int nbits = 0;
     while (nbits < 33 && (n >> nbits)) ++nbits;
     int end_bit = std::max(1, std::min(64, 2 * nbits));
     uint64_t nuniq = 0;
     if (nkeys) {
         size_t tmp = 0;
-        G2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.as<u64>(), keys2.as<u64>(), (int)nkeys, 0, end_bit, st->stream));
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.as<u64>(), keys2.as<u64>(), (int64_t)nkeys, 0,
+                                                end_bit, st->stream));
         G2M_TRY(st->cub_tmp.ensure(tmp));
-        G2M_CUDA(cub::DeviceRadixSort::SortKeys(st->cub_tmp.p, tmp, keys.as<u64>(), keys2.as<u64>(), (int)nkeys, 0, end_bit, st->stream));
+        G2M_CUDA(cub::DeviceRadixSort::SortKeys(st->cub_tmp.p, tmp, keys.as<u64>(), keys2.as<u64>(), (int64_t)nkeys,
+                                                0, end_bit, st->stream));
         size_t tmp2 = 0;
-        G2M_CUDA(cub::DeviceSelect::Unique(nullptr, tmp2, keys2.as<u64>(), keys.as<u64>(), nk.as<u64>() + 1, (int)nkeys, st->stream));
+        G2M_CUDA(cub::DeviceSelect::Unique(nullptr, tmp2, keys2.as<u64>(), keys.as<u64>(), nk.as<u64>() + 1,
+                                           (int64_t)nkeys, st->stream));
         G2M_TRY(st->cub_tmp.ensure(tmp2));
-        G2M_CUDA(cub::DeviceSelect::Unique(st->cub_tmp.p, tmp2, keys2.as<u64>(), keys.as<u64>(), nk.as<u64>() + 1, (int)nkeys, st->stream));
+        G2M_CUDA(cub::DeviceSelect::Unique(st->cub_tmp.p, tmp2, keys2.as<u64>(), keys.as<u64>(), nk.as<u64>() + 1,
+                                           (int64_t)nkeys, st->stream));
         G2M_CUDA(cudaMemcpyAsync(&nuniq, nk.as<u64>() + 1, 8, cudaMemcpyDeviceToHost, st->stream));
         G2M_CUDA(cudaStreamSynchronize(st->stream));
     }
+    keys2.release();
+    if (nuniq > 0xffffffffull * 4) return fail(G2M_EUSAGE, "graph too large");
     auto g = std::make_unique<g2m_graph>();
     g->dev = device;
     g->nv = n;
     g->slots = nuniq;
+    DevBuf cnt;
+    G2M_TRY(cnt.ensure(std::max<uint64_t>(n, 1) * 8));
+    G2M_CUDA(cudaMemsetAsync(cnt.p, 0, std::max<uint64_t>(n, 1) * 8, st->stream));
     G2M_TRY(g->off.ensure((n + 1) * 8));
     G2M_TRY(g->nbr.ensure(std::max<uint64_t>(nuniq, 1) * 4));
     if (nuniq) {
-        k_keys_to_csr<<<grid_for(st, nuniq, 256), 256, 0, st->stream>>>(keys.as<u64>(), nuniq, n, g->nbr.as<u32>(), cnt.as<u64>());
+        k_keys_to_csr<<<grid_for(st, nuniq, 256), 256, 0, st->stream>>>(keys.as<u64>(), nuniq, n, g->nbr.as<u32>(),
+                                                                          cnt.as<u64>());
         G2M_CUDA(cudaGetLastError());
     }
     G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), g->off.as<u64>(), n));
@@ -556,6 +589,58 @@ extern "C" int g2m_graph_from_edges(int32_t device, const int64_t* edges, uint64
     G2M_TRY(finish_graph(g.get(), st));
     *out = g.release();
     return G2M_OK;
+}
+
+extern "C" int g2m_graph_from_edges(int32_t device, const int64_t* edges, uint64_t m,
+                                    uint64_t num_vertices, const uint32_t* labels, g2m_graph** out) {
+    if (!out) return fail(G2M_EUSAGE, "null output handle");
+    DevState* st;
+    G2M_TRY(dev_state(device, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(device));
+    const uint64_t n = num_vertices;
+    DevBuf din, keys, keys2, nk;
+    G2M_TRY(din.ensure(std::max<uint64_t>(m, 1) * 16));
+    G2M_TRY(keys.ensure(std::max<uint64_t>(2 * m, 1) * 8));
+    G2M_TRY(keys2.ensure(std::max<uint64_t>(2 * m, 1) * 8));
+    G2M_TRY(nk.ensure(16));
+    G2M_CUDA(cudaMemsetAsync(nk.p, 0, 16, st->stream));
+    if (m) {
+        G2M_CUDA(cudaMemcpyAsync(din.p, edges, m * 16, cudaMemcpyHostToDevice, st->stream));
+        ++st->launches;
+        k_edge_keys<<<grid_for(st, m, 256), 256, 0, st->stream>>>(din.as<i64>(), m, n, keys.as<u64>(), nk.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    uint64_t nkeys = 0;
+    G2M_CUDA(cudaMemcpyAsync(&nkeys, nk.p, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    din.release();
+    return keys_to_graph(st, device, n, keys, keys2, nk, nkeys, labels, out);
+}
+
+extern "C" int g2m_graph_rmat(int32_t device, int32_t scale, int32_t edgefactor, uint64_t seed, double a,
+                              double b, double c, g2m_graph** out) {
+    if (!out) return fail(G2M_EUSAGE, "null output handle");
+    if (scale < 1 || scale > 31 || edgefactor < 1) return fail(G2M_EUSAGE, "bad R-MAT scale / edge factor");
+    if (a < 0 || b < 0 || c < 0 || a + b + c > 1) return fail(G2M_EUSAGE, "bad R-MAT probabilities");
+    DevState* st;
+    G2M_TRY(dev_state(device, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(device));
+    const uint64_t n = (uint64_t)1 << scale;
+    const uint64_t m = (uint64_t)edgefactor << scale;
+    DevBuf keys, keys2, nk;
+    G2M_TRY(keys.ensure(2 * m * 8));
+    G2M_TRY(keys2.ensure(2 * m * 8));
+    G2M_TRY(nk.ensure(16));
+    G2M_CUDA(cudaMemsetAsync(nk.p, 0, 16, st->stream));
+    ++st->launches;
+    k_rmat_keys<<<st->sms * 16, 256, 0, st->stream>>>(m, scale, seed, a, b, c, n, keys.as<u64>(), nk.as<u64>());
+    G2M_CUDA(cudaGetLastError());
+    uint64_t nkeys = 0;
+    G2M_CUDA(cudaMemcpyAsync(&nkeys, nk.p, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return keys_to_graph(st, device, n, keys, keys2, nk, nkeys, nullptr, out);
 }
 
 // ---- reduced edge-task offsets: row v holds |N(v) ∩ [0, v)| tasks (graph.py:275-286)
@@ -1325,6 +1410,10 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     int sm_smem = 0;
     G2M_CUDA(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0));
     DevBuf slab;   // global rows of the GR tier
+    // G2M_DIRECT_MAX: widest window (bits) for the direct bitmap (tests force
+    // the two-level window / hash paths with small values)
+    const u32 direct_max = getenv("G2M_DIRECT_MAX") ? (u32)strtoul(getenv("G2M_DIRECT_MAX"), nullptr, 10)
+                                                     : 0xffffffffu;
     auto cta = [&](auto wtag, auto nwtag, auto grtag, int cls, int want_ctas) -> int {
         constexpr int W = decltype(wtag)::value;
         constexpr int NW = decltype(nwtag)::value;
@@ -1333,7 +1422,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         // window bitmap: as wide as the widest source of the class needs, within
         // the shared memory left at `want_ctas` blocks per SM
         const size_t base = cta_smem_bytes(K, W, NW, 0, GR, SUP);
-        const size_t per_block = std::min<size_t>((size_t)max_smem, (size_t)sm_smem / want_ctas - 1024);
+        const size_t per_block = std::min<size_t>((size_t)max_smem, (size_t)sm_smem / want_ctas - 2048);
         u32 bmw = 0;
         if (per_block > base + 64) bmw = (u32)std::min<size_t>((per_block - base) / 6, ((size_t)spans[cls] + 31) / 32);
         bmw &= ~1u;
@@ -1358,7 +1447,8 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         G2M_TRY(timed([&] {
             ++st->launches;
             kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
-                                                                 next + slot, count, bmw, grows, tsup, split);
+                                                                 next + slot, count, bmw, grows, tsup, split,
+                                                                 direct_max);
         }));
         ++slot;
         return G2M_OK;

@@ -491,3 +491,56 @@ def test_kmotif_bfs_log_and_counts():
                                   cfg=EX.ExecutionConfig(search="dfs")))
     assert not dfs.applied("bounded-bfs")
     assert res.counts == dfs.counts
+
+
+def _rmat_device_host_restatement(scale, ef, seed, a=0.57, b=0.19, c=0.19):
+    """numpy restatement of k_rmat_keys (g2m.cu): splitmix-style hash of
+    (seed, edge, bit) -> uniform double -> quadrant bits."""
+    m = ef << scale
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+    i = np.arange(m, dtype=np.uint64)
+    u = np.zeros(m, dtype=np.uint64)
+    v = np.zeros(m, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for bit in range(scale):
+            z = (np.uint64(seed) * np.uint64(0x9E3779B97F4A7C15) + i * np.uint64(0xD1B54A32D192ED03)
+                 + np.uint64(bit) * np.uint64(0xABC98388FB8FAC03)) & M
+            z ^= z >> np.uint64(30); z = (z * np.uint64(0xBF58476D1CE4E5B9)) & M
+            z ^= z >> np.uint64(27); z = (z * np.uint64(0x94D049BB133111EB)) & M
+            z ^= z >> np.uint64(31)
+            r = (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+            u |= (r >= a + b).astype(np.uint64) << np.uint64(bit)
+            v |= (((r >= a) & (r < a + b)) | (r >= a + b + c)).astype(np.uint64) << np.uint64(bit)
+    return np.column_stack([u.astype(np.int64), v.astype(np.int64)])
+
+
+def test_device_rmat_generator_equals_host_restatement():
+    g = GR.rmat_device(11, 8, 3)
+    h = GR.from_edges(_rmat_device_host_restatement(11, 8, 3), num_vertices=1 << 11)
+    assert g == h and g.max_degree == h.max_degree
+    want = pm.triangle_count(h)
+    assert pm.triangle_count(g) == want
+
+
+@pytest.mark.parametrize("direct_max", ["0", "4096"])
+def test_lgs_two_level_window_matches(monkeypatch, direct_max):
+    """Windows too wide for the direct bitmap use the two-level window (or the
+    hash map): forced here by capping the direct bitmap."""
+    g = GR.from_edges(G.rmat_edges(14, 16, 3), num_vertices=1 << 14)
+    og = GR.orient(g)
+    want = {}
+    for k in (3, 4, 5):
+        f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
+        want[k] = EX.execute(og, f, EX._default_tasks(og, f), lgs=False)[0]
+    monkeypatch.setenv("G2M_DIRECT_MAX", direct_max)
+    for k in (3, 4, 5):
+        f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
+        assert EX.execute(og, f, EX._default_tasks(og, f))[0] == want[k], k
+    # the diamond support path shares the CTA kernels
+    pl = make_plan(diamond(), g, rewrite=True)
+    fd = PL.as_forest(pl)
+    td = EX._default_tasks(g, fd)
+    monkeypatch.delenv("G2M_DIRECT_MAX")
+    wd = EX.execute(g, fd, td, lgs=False)[0]
+    monkeypatch.setenv("G2M_DIRECT_MAX", direct_max)
+    assert EX.execute(g, fd, td)[0] == wd
