@@ -420,8 +420,8 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
         cp = compile_forest(forest, False, False, dg.max_degree, flatten=flatten)
         spec = N.TaskSpec()
         spec.kind = N.TASKS_VERTEX
-        if rr is not None:
-            spec.rr_chunk, spec.rr_parts, spec.rr_part = rr
+        if rr is not None:   # sources of very different weight: deal them one by one
+            spec.rr_chunk, spec.rr_parts, spec.rr_part = 1, rr[1], rr[2]
         words = np.zeros(2, dtype=np.uint64)
         stats = N.RunStats()
         cfg = run_config if run_config is not None else N.RunConfig()
@@ -432,8 +432,8 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
     if lgs and not instrument and _is_cycle4_count(g, forest, tasks, sink, index):
         spec = N.TaskSpec()
         spec.kind = N.TASKS_VERTEX
-        if rr is not None:
-            spec.rr_chunk, spec.rr_parts, spec.rr_part = rr
+        if rr is not None:   # top vertices of very different weight: deal them one by one
+            spec.rr_chunk, spec.rr_parts, spec.rr_part = 1, rr[1], rr[2]
         words = np.zeros(2, dtype=np.uint64)
         stats = N.RunStats()
         cfg = run_config if run_config is not None else N.RunConfig()
