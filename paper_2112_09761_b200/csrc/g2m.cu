@@ -1464,10 +1464,10 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 32>{}, F{}, 5, 1));
     else if constexpr (K == 5)
         G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 24>{}, F{}, 5, 1));
-    else
-        G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, F{}, 5, 1));
+    else   // k = 3: no rows; two blocks per SM, windows beyond the bitmap go two-level
+        G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, F{}, 5, 2));
     if constexpr (K == 3)
-        G2M_TRY(cta(integral_constant<int, 64>{}, integral_constant<int, 16>{}, F{}, 7, 1));
+        G2M_TRY(cta(integral_constant<int, 64>{}, integral_constant<int, 32>{}, F{}, 7, 1));
     else
         G2M_TRY(cta(integral_constant<int, 32>{}, integral_constant<int, 16>{}, std::true_type{}, 7, 1));
     return G2M_OK;
