@@ -261,12 +261,14 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
 // -- d(d-1)/2 lane-parallel tests instead of streaming the out-lists of A,
 // which for small sources are mostly far longer than A itself.
 // ---------------------------------------------------------------------------
-template <int K, int WPB>
+template <int K, int WPB, int MAXD = 64>
 __global__ void __launch_bounds__(WPB * 32)
 k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
                u64 nverts, u64* next, u64 grab, u64* count) {
-    __shared__ u32 sA[WPB][64];
-    __shared__ __align__(8) u64 sR[WPB][64];
+    static_assert(K == 3 || MAXD <= 64 || (K == 4 && MAXD <= 128), "row width");
+    constexpr int RW = MAXD > 64 ? 2 : 1;      // u64 words per local row
+    __shared__ u32 sA[WPB][MAXD];
+    __shared__ __align__(8) u64 sR[WPB][K > 3 ? MAXD * RW : 1];
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
     u32* A = sA[w];
@@ -282,10 +284,10 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
             const u32 u = __ldg(verts + t);
             const u64 b = __ldg(off + u);
             const u32 d = (u32)(__ldg(off + u + 1) - b);
-            A[lane] = lane < d ? __ldg(nbr + b + lane) : 0u;
-            A[lane + 32] = lane + 32 < d ? __ldg(nbr + b + lane + 32) : 0u;
-            R[lane] = 0;
-            R[lane + 32] = 0;
+#pragma unroll
+            for (u32 x = lane; x < (u32)MAXD; x += 32) A[x] = x < d ? __ldg(nbr + b + x) : 0u;
+            if constexpr (K > 3)
+                for (u32 x = lane; x < (u32)(MAXD * RW); x += 32) R[x] = 0;
             __syncwarp();
             const u32 np = d * (d - 1) / 2;
             const float D = 2.f * (float)d - 1.f;
@@ -299,13 +301,30 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
                 const u64 ao = __ldg(off + a);
                 if (g2m_has_g(nbr + ao, (u32)(__ldg(off + a + 1) - ao), A[j])) {
                     if constexpr (K == 3) acc += 1;
-                    else atomicOr((u32*)(R + i) + (j >> 5), 1u << (j & 31u));
+                    else atomicOr((u32*)(R + i * RW) + (j >> 5), 1u << (j & 31u));
                 }
             }
-            if constexpr (K > 3) {
+            if constexpr (K > 3 && RW == 1) {
                 __syncwarp();
                 if (lane < d) acc += Chain1<K - 2>::run(R, R[lane]);
                 if (lane + 32 < d) acc += Chain1<K - 2>::run(R, R[lane + 32]);
+            } else if constexpr (K == 4) {   // two-word rows: Σ_i Σ_{j in R_i} |R_i & R_j|
+                __syncwarp();
+                for (u32 i = lane; i < d; i += 32) {
+                    const u64 r0 = R[2 * i], r1 = R[2 * i + 1];
+                    u64 it = r0;
+                    while (it) {
+                        const int j = __ffsll(it) - 1;
+                        it &= it - 1;
+                        acc += (u64)__popcll(r0 & R[2 * j]) + (u64)__popcll(r1 & R[2 * j + 1]);
+                    }
+                    it = r1;
+                    while (it) {
+                        const int j = 64 + __ffsll(it) - 1;
+                        it &= it - 1;
+                        acc += (u64)__popcll(r1 & R[2 * j + 1]);
+                    }
+                }
             }
             __syncwarp();
         }
@@ -460,8 +479,14 @@ __device__ __forceinline__ u32 cta_probe(const u64* __restrict__ off, const u32*
 // compacted again and shared by the whole warp.
 // bmw: u32 words of the window bitmap (0 = hash only).
 // ---------------------------------------------------------------------------
+// Blocks per SM the narrow tiers are launched at (g2m.cu): keeps the register
+// budget at what that occupancy allows (the window/hash variants add live values).
+__host__ __device__ constexpr int cta_min_blocks(int K, int W) {
+    return K == 3 ? (W <= 16 ? 4 : 1) : (K == 4 ? (W <= 8 ? 3 : 1) : (W == 4 ? 2 : (W <= 8 ? 3 : 1)));
+}
+
 template <int K, int W, int NW, bool GR = false, bool SUP = false>
-__global__ void __launch_bounds__(NW * 32)
+__global__ void __launch_bounds__(NW * 32, cta_min_blocks(K, W))
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
              u64 nverts, u64* next, u64* count, u32 bmw, u64* grows, u32* tsup, u32 split, u32 direct_max) {
     constexpr u32 CH = 4;             // words compacted per round (<= 256 candidates)

@@ -1364,6 +1364,15 @@ static u64 pair_maxd() {
     return v;
 }
 
+// k = 3, 4 take the pair tier further (G2M_PAIR_MAXD3, <= 128; two-word rows for k = 4).
+static u64 pair_maxd3() {
+    static const u64 v = [] {
+        const char* e = getenv("G2M_PAIR_MAXD3");
+        return e ? std::min<u64>(strtoull(e, nullptr, 10), 128) : (u64)128;
+    }();
+    return v;
+}
+
 template <int K, bool SUP = false>
 static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const u32* lists, u64 stride,
                              const uint64_t* sizes, const uint32_t* spans, u64* ctr, double* kms,
@@ -1390,8 +1399,12 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         u64 grab = std::max<u64>(1, std::min<u64>(16, sizes[8] / ((u64)st->sms * 64 * WPB)));
         G2M_TRY(timed([&] {
             ++st->launches;
-            k_clique_pairs<K, WPB><<<st->sms * 8, WPB * 32, 0, st->stream>>>(off, nbr, lists + 8 * stride, sizes[8],
-                                                                             next + slot, grab, count);
+            if constexpr (K <= 4)
+                k_clique_pairs<K, WPB, 128><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
+            else
+                k_clique_pairs<K, WPB><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
         }));
         ++slot;
     }
@@ -1514,7 +1527,8 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     if (g->nv) {
         ++st->launches;
         g2m_clique::k_clique_bucket<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(
-            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 2048, pair_maxd(), rr_chunk, parts, pt, st->tasks_b.as<u32>(),
+            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 2048, k <= 4 ? pair_maxd3() : pair_maxd(), rr_chunk, parts, pt,
+            st->tasks_b.as<u32>(),
             stride, dsizes, dspans);
         G2M_CUDA(cudaGetLastError());
     }
