@@ -1373,6 +1373,14 @@ static u64 pair_maxd3() {
     return v;
 }
 
+// Triangle counting (no rows) takes the pair tier furthest (G2M_PAIR_MAXD_TC,
+// <= 256): to 128 while the CTA tiers' id windows fit their shared-memory
+// bitmaps, to 256 on graphs large enough that they do not (> 2^24 vertices).
+static u64 pair_maxd_tc(u64 nv) {
+    if (const char* e = getenv("G2M_PAIR_MAXD_TC")) return std::min<u64>(strtoull(e, nullptr, 10), 256);
+    return nv > ((u64)1 << 24) ? 256 : 128;
+}
+
 template <int K, bool SUP = false>
 static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const u32* lists, u64 stride,
                              const uint64_t* sizes, const uint32_t* spans, u64* ctr, double* kms,
@@ -1399,7 +1407,10 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         u64 grab = std::max<u64>(1, std::min<u64>(16, sizes[8] / ((u64)st->sms * 64 * WPB)));
         G2M_TRY(timed([&] {
             ++st->launches;
-            if constexpr (K <= 4)
+            if constexpr (K == 3)
+                k_clique_pairs<K, WPB, 256><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
+            else if constexpr (K == 4)
                 k_clique_pairs<K, WPB, 128><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
                     off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
             else
@@ -1527,7 +1538,8 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     if (g->nv) {
         ++st->launches;
         g2m_clique::k_clique_bucket<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(
-            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 2048, k <= 4 ? pair_maxd3() : pair_maxd(), rr_chunk, parts, pt,
+            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 2048,
+            k == 3 ? pair_maxd_tc(g->nv) : (k == 4 ? pair_maxd3() : pair_maxd()), rr_chunk, parts, pt,
             st->tasks_b.as<u32>(),
             stride, dsizes, dspans);
         G2M_CUDA(cudaGetLastError());
