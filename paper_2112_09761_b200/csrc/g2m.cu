@@ -162,6 +162,7 @@ struct DevState {
     DevBuf tmp1, tmp2;       // grow-only scratch of the preprocessing passes (rank relabelling)
     DevBuf frontier;         // BFS level-3 frontier items (grow-only)
     DevBuf c4slab;           // 4-cycle staging slabs, one per block
+    DevBuf hubs;             // [0] = count, then the hub rows of a row pass (rows longer than kHubRow)
 };
 
 static std::mutex g_dev_mu;
@@ -351,12 +352,38 @@ __device__ __forceinline__ bool orient_keep(u32 du, u32 u, u32 dw, u32 w) {
     return du < dw || (du == dw && u < w);
 }
 
-__global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u64 nv, u64* cnt) {
+// Row passes run one warp per row. Rows longer than kHubRow (the hubs of a
+// skewed graph: up to ~10^6 slots) would serialise the whole pass on one
+// warp, so the warp pass appends them to a list and a second kernel gives
+// each hub a 1024-thread block.
+constexpr u32 kHubRow = 2048;
+constexpr int kHubThreads = 1024;
+
+__device__ __forceinline__ void push_hub(u32* hubs, u32 u) {
+    hubs[1 + atomicAdd(hubs, 1u)] = u;
+}
+
+// Block-wide sum (kHubThreads threads); result valid in every thread.
+__device__ __forceinline__ u64 block_sum_hub(u64 v, u64* red) {
+    v = g2m_wsum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    u64 t = 0;
+    for (int w = 0; w < kHubThreads / 32; ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+__global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u64 nv, u64* cnt, u32* hubs) {
     const u32 lane = g2m_lane();
     for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
          u += ((u64)gridDim.x * blockDim.x) >> 5) {
         const u64 b = off[u], e = off[u + 1];
         const u32 du = (u32)(e - b);
+        if (du > kHubRow) {
+            if (lane == 0) push_hub(hubs, (u32)u);
+            continue;
+        }
         u32 c = 0;
         for (u64 base = b; base < e; base += 32) {
             const u64 i = base + lane;
@@ -369,12 +396,31 @@ __global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u
     }
 }
 
+__global__ void __launch_bounds__(kHubThreads)
+k_orient_count_hubs(const u64* off, const u32* nbr, const u32* deg, const u32* hubs, u64* cnt) {
+    __shared__ u64 red[kHubThreads / 32];
+    const u32 nh = hubs[0];
+    for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
+        const u32 u = hubs[1 + h];
+        const u64 b = off[u], e = off[u + 1];
+        const u32 du = (u32)(e - b);
+        u64 c = 0;
+        for (u64 i = b + threadIdx.x; i < e; i += kHubThreads) {
+            const u32 x = __ldg(nbr + i);
+            c += orient_keep(du, u, __ldg(deg + x), x) ? 1 : 0;
+        }
+        c = block_sum_hub(c, red);
+        if (threadIdx.x == 0) cnt[u] = c;
+    }
+}
+
 __global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* deg, u64 nv, const u64* noff, u32* out) {
     const u32 lane = g2m_lane();
     for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
          u += ((u64)gridDim.x * blockDim.x) >> 5) {
         const u64 b = off[u], e = off[u + 1];
         const u32 du = (u32)(e - b);
+        if (du > kHubRow) continue;   // k_orient_fill_hubs
         u64 w = noff[u];
         for (u64 base = b; base < e; base += 32) {
             const u64 i = base + lane;
@@ -385,6 +431,49 @@ __global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* deg, u6
             w += __popc(m);
         }
     }
+}
+
+// Ordered compaction of a hub row: 1024-slot steps, warp ballots, warp
+// offsets from a shared prefix.
+__global__ void __launch_bounds__(kHubThreads)
+k_orient_fill_hubs(const u64* off, const u32* nbr, const u32* deg, const u32* hubs, const u64* noff, u32* out) {
+    __shared__ u32 wc[kHubThreads / 32];
+    const u32 lane = g2m_lane(), wid = threadIdx.x >> 5;
+    const u32 nh = hubs[0];
+    for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
+        const u32 u = hubs[1 + h];
+        const u64 b = off[u], e = off[u + 1];
+        const u32 du = (u32)(e - b);
+        u64 w = noff[u];
+        for (u64 base = b; base < e; base += kHubThreads) {
+            const u64 i = base + threadIdx.x;
+            const u32 x = i < e ? __ldg(nbr + i) : 0u;
+            const bool k = i < e && orient_keep(du, u, __ldg(deg + x), x);
+            const u32 m = __ballot_sync(G2M_FULL, k);
+            if (lane == 0) wc[wid] = __popc(m);
+            __syncthreads();
+            u32 before = 0, tot = 0;
+            for (u32 q = 0; q < kHubThreads / 32; ++q) {
+                const u32 c = wc[q];
+                before += q < wid ? c : 0u;
+                tot += c;
+            }
+            if (k) out[w + before + __popc(m & g2m_lanemask_lt())] = x;
+            w += tot;
+            __syncthreads();
+        }
+    }
+}
+
+static int hub_list(DevState* st, uint64_t slots, u32** out) {
+    G2M_TRY(st->hubs.ensure((slots / kHubRow + 2) * 4));
+    G2M_CUDA(cudaMemsetAsync(st->hubs.p, 0, 4, st->stream));
+    *out = st->hubs.as<u32>();
+    return G2M_OK;
+}
+
+static int hub_grid(DevState* st, uint64_t slots) {
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(slots / kHubRow + 1, (uint64_t)st->sms * 2));
 }
 
 static int exclusive_scan_u64(DevState* st, const u64* in, u64* out, uint64_t n) {
@@ -403,36 +492,54 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     o->dev = g->dev;
     o->nv = g->nv;
     o->oriented = 1;
+    const bool dbg = getenv("G2M_DEBUG") != nullptr;
+    auto tr = Clock::now();
+    auto phase = [&](const char* what) {
+        if (!dbg) return;
+        cudaStreamSynchronize(st->stream);
+        fprintf(stderr, "[g2m] orient %s: %.2f ms\n", what, ms_since(tr));
+        tr = Clock::now();
+    };
     G2M_TRY(o->off.ensure((g->nv + 1) * 8));
     DevBuf& cnt = st->tmp1;   // grow-only scratch (the caller holds the device lock)
     DevBuf& deg = st->tmp2;
+    u32* hubs = nullptr;
     G2M_TRY(cnt.ensure(std::max<uint64_t>(g->nv, 1) * 8));
     G2M_TRY(deg.ensure(std::max<uint64_t>(g->nv, 1) * 4));
     if (g->nv) {
         ++st->launches;
         k_degrees<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, deg.as<u32>());
         int grid = grid_for(st, g->nv * 32, 256);
-        ++st->launches;
+        G2M_TRY(hub_list(st, g->slots, &hubs));
+        st->launches += 2;
         k_orient_count<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv,
-                                                      cnt.as<u64>());
+                                                      cnt.as<u64>(), hubs);
+        k_orient_count_hubs<<<hub_grid(st, g->slots), kHubThreads, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), hubs, cnt.as<u64>());
         G2M_CUDA(cudaGetLastError());
     }
+    phase("degrees+count");
     G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), o->off.as<u64>(), g->nv));
     G2M_CUDA(cudaMemcpyAsync(&o->slots, o->off.as<u64>() + g->nv, 8, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
+    phase("scan");
     G2M_TRY(o->nbr.ensure(std::max<uint64_t>(o->slots, 1) * 4));
     if (g->nv) {
         int grid = grid_for(st, g->nv * 32, 256);
-        ++st->launches;
+        st->launches += 2;
         k_orient_fill<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv,
                                                      o->off.as<u64>(), o->nbr.as<u32>());
+        k_orient_fill_hubs<<<hub_grid(st, g->slots), kHubThreads, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), hubs, o->off.as<u64>(), o->nbr.as<u32>());
         G2M_CUDA(cudaGetLastError());
     }
     if (g->labels.p) {
         G2M_TRY(o->labels.ensure(std::max<uint64_t>(g->nv, 1) * 4));
         G2M_CUDA(cudaMemcpyAsync(o->labels.p, g->labels.p, g->nv * 4, cudaMemcpyDeviceToDevice, st->stream));
     }
+    phase("alloc+fill");
     G2M_TRY(finish_graph(o.get(), st));
+    phase("max degree");
     *out = o.release();
     return G2M_OK;
 }
@@ -713,15 +820,138 @@ __global__ void k_rank_scatter(const u64* off, const u64* sorted, u64 nv, u32* r
 
 // (new row << rb | new column) per slot (ids < 2^rb); one radix sort puts
 // every row's columns in ascending order.
-__global__ void k_rank_keys64(const u64* off, const u32* nbr, u64 nv, const u32* rank, int rb, u64* keys) {
+__global__ void k_rank_keys64(const u64* off, const u32* nbr, u64 nv, const u32* rank, int rb, u64* keys,
+                              u32* hubs) {
     const u32 lane = g2m_lane();
     for (u64 v = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; v < nv;
          v += ((u64)gridDim.x * blockDim.x) >> 5) {
         const u64 b = off[v], e = off[v + 1];
         if (b == e) continue;
+        if (e - b > kHubRow) {
+            if (lane == 0) push_hub(hubs, (u32)v);
+            continue;
+        }
         const u64 hi = (u64)rank[v] << rb;
         for (u64 i = b + lane; i < e; i += 32) keys[i] = hi | __ldg(rank + __ldg(nbr + i));
     }
+}
+
+__global__ void __launch_bounds__(kHubThreads)
+k_rank_keys64_hubs(const u64* off, const u32* nbr, const u32* rank, int rb, u64* keys, const u32* hubs) {
+    const u32 nh = hubs[0];
+    for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
+        const u32 v = hubs[1 + h];
+        const u64 b = off[v], e = off[v + 1];
+        const u64 hi = (u64)rank[v] << rb;
+        for (u64 i = b + threadIdx.x; i < e; i += kHubThreads) keys[i] = hi | __ldg(rank + __ldg(nbr + i));
+    }
+}
+
+// ---- per-row rank-space fill + sort (replaces the global key sort) --------
+// Row r = rank[v] of the rank-space CSR holds rank[w] for w in N(v), sorted.
+// Rows of <= 32 are sorted in registers (warp bitonic), rows of <= 1024 in a
+// per-warp shared buffer, longer rows by one 1024-thread block per row in
+// shared memory (<= kRowSortBlock), and the few longer still by a segmented
+// radix sort over just those rows.
+constexpr u32 kRowSortWarp = 1024;
+constexpr u32 kRowSortBlock = 8192;
+constexpr int kFillWarps = 8;
+
+__device__ __forceinline__ u32 bitonic32(u32 x, u32 lane) {
+#pragma unroll
+    for (u32 k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            const u32 y = __shfl_xor_sync(G2M_FULL, x, j);
+            const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+            x = (lower == up) ? min(x, y) : max(x, y);
+        }
+    return x;
+}
+
+// Bitonic sort of s[0, P) (P a power of two) by `nt` threads with index t;
+// sync() separates the stages.
+template <typename Sync>
+__device__ __forceinline__ void bitonic_smem(u32* s, u32 P, u32 t, u32 nt, Sync&& sync) {
+    for (u32 k = 2; k <= P; k <<= 1)
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            for (u32 i = t; i < P / 2; i += nt) {
+                const u32 lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));   // i-th pair (lo, lo ^ j)
+                const u32 hi = lo | j;
+                const u32 a = s[lo], b = s[hi];
+                const bool asc = (lo & k) == 0;
+                if ((a > b) == asc) { s[lo] = b; s[hi] = a; }
+            }
+            sync();
+        }
+}
+
+__global__ void __launch_bounds__(kFillWarps * 32)
+k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* rk_off, u32* rk_nbr, u32* hubs) {
+    __shared__ u32 buf[kFillWarps][kRowSortWarp];
+    const u32 lane = g2m_lane();
+    u32* sb = buf[threadIdx.x >> 5];
+    for (u64 v = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; v < nv;
+         v += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u64 b = off[v], e = off[v + 1];
+        const u32 d = (u32)(e - b);
+        if (d == 0) continue;
+        if (d > kRowSortWarp) {
+            if (lane == 0) push_hub(hubs, (u32)v);
+            continue;
+        }
+        u32* out = rk_nbr + rk_off[rank[v]];
+        if (d <= 32) {
+            u32 x = lane < d ? __ldg(rank + __ldg(nbr + b + lane)) : 0xffffffffu;
+            x = bitonic32(x, lane);
+            if (lane < d) out[lane] = x;
+            continue;
+        }
+        const u32 P = 1u << (32 - __clz(d - 1));
+        for (u32 i = lane; i < P; i += 32) sb[i] = i < d ? __ldg(rank + __ldg(nbr + b + i)) : 0xffffffffu;
+        __syncwarp();
+        bitonic_smem(sb, P, lane, 32, [] { __syncwarp(); });
+        for (u32 i = lane; i < d; i += 32) out[i] = sb[i];
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kHubThreads)
+k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_off, u32* rk_nbr, const u32* hubs,
+                 u32* big) {
+    __shared__ u32 sb[kRowSortBlock];
+    const u32 nh = hubs[0];
+    for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
+        const u32 v = hubs[1 + h];
+        const u64 b = off[v];
+        const u32 d = (u32)(off[v + 1] - b);
+        const u32 r = rank[v];
+        u32* out = rk_nbr + rk_off[r];
+        if (d > kRowSortBlock) {   // unsorted; sorted by the segmented pass
+            for (u32 i = threadIdx.x; i < d; i += kHubThreads) out[i] = __ldg(rank + __ldg(nbr + b + i));
+            if (threadIdx.x == 0) push_hub(big, r);
+            continue;
+        }
+        const u32 P = 1u << (32 - __clz(d - 1));
+        for (u32 i = threadIdx.x; i < P; i += kHubThreads) sb[i] = i < d ? __ldg(rank + __ldg(nbr + b + i)) : 0xffffffffu;
+        __syncthreads();
+        bitonic_smem(sb, P, threadIdx.x, kHubThreads, [] { __syncthreads(); });
+        for (u32 i = threadIdx.x; i < d; i += kHubThreads) out[i] = sb[i];
+        __syncthreads();
+    }
+}
+
+__global__ void k_big_segments(const u32* big, const u64* rk_off, u64* beg, u64* end) {
+    const u32 n = big[0];
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        beg[i] = rk_off[big[1 + i]];
+        end[i] = rk_off[big[1 + i] + 1];
+    }
+}
+
+__global__ void k_copy_segments(const u32* src, u32* dst, const u64* beg, const u64* end, u32 n) {
+    for (u32 s = blockIdx.x; s < n; s += gridDim.x)
+        for (u64 i = beg[s] + threadIdx.x; i < end[s]; i += blockDim.x) dst[i] = src[i];
 }
 
 __global__ void k_low_bits(const u64* keys, u64 n, int rb, u32* out) {
@@ -780,16 +1010,63 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     }
     phase("keys+sort+scatter");
     G2M_TRY(exclusive_scan_u64(st, rdeg.as<u64>(), g->rk_off.as<u64>(), nv));
-    if (nv && slots) {
+    if (nv && slots && !getenv("G2M_RANK_RADIX")) {
+        // rows written in place and sorted per row
+        u32* hubs = nullptr;
+        G2M_TRY(hub_list(st, slots, &hubs));
+        DevBuf bigl;
+        G2M_TRY(bigl.ensure((slots / kRowSortBlock + 2) * 4));
+        G2M_CUDA(cudaMemsetAsync(bigl.p, 0, 4, st->stream));
+        st->launches += 2;
+        k_rank_fill<<<grid_for(st, nv * 32, kFillWarps * 32), kFillWarps * 32, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), nv, rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs);
+        k_rank_fill_hubs<<<hub_grid(st, slots), kHubThreads, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs,
+            bigl.as<u32>());
+        G2M_CUDA(cudaGetLastError());
+        phase("fill+row sort");
+        u32 nbig = 0;
+        G2M_CUDA(cudaMemcpyAsync(&nbig, bigl.p, 4, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        if (nbig) {
+            DevBuf segs;
+            G2M_TRY(segs.ensure((u64)nbig * 16));
+            u64* beg = segs.as<u64>();
+            u64* end = beg + nbig;
+            ++st->launches;
+            k_big_segments<<<grid_for(st, nbig, 256), 256, 0, st->stream>>>(bigl.as<u32>(), g->rk_off.as<u64>(), beg,
+                                                                           end);
+            G2M_TRY(st->tmp1.ensure(slots * 4));
+            u32* sorted_out = st->tmp1.as<u32>();
+            int rb = 1;
+            while (rb < 32 && ((u64)1 << rb) < nv) ++rb;
+            size_t tb = 0;
+            G2M_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tb, g->rk_nbr.as<u32>(), sorted_out,
+                                                             (int64_t)slots, (int64_t)nbig, beg, end, 0, rb,
+                                                             st->stream));
+            G2M_TRY(st->cub_tmp.ensure(tb));
+            G2M_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(st->cub_tmp.p, tb, g->rk_nbr.as<u32>(), sorted_out,
+                                                             (int64_t)slots, (int64_t)nbig, beg, end, 0, rb,
+                                                             st->stream));
+            ++st->launches;
+            k_copy_segments<<<std::min<u32>(nbig, st->sms * 4), 1024, 0, st->stream>>>(sorted_out, g->rk_nbr.as<u32>(),
+                                                                                      beg, end, nbig);
+            G2M_CUDA(cudaGetLastError());
+        }
+    } else if (nv && slots) {
         int rb = 1;
         while (rb < 32 && ((u64)1 << rb) < nv) ++rb;
         G2M_TRY(st->tmp1.ensure(slots * 8));   // grow-only device scratch, no malloc per call
         G2M_TRY(st->tmp2.ensure(slots * 8));
         u64* k64 = st->tmp1.as<u64>();
         u64* s64 = st->tmp2.as<u64>();
-        ++st->launches;
+        u32* hubs = nullptr;
+        G2M_TRY(hub_list(st, slots, &hubs));
+        st->launches += 2;
         k_rank_keys64<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), nv,
-                                                                            rank.as<u32>(), rb, k64);
+                                                                            rank.as<u32>(), rb, k64, hubs);
+        k_rank_keys64_hubs<<<hub_grid(st, slots), kHubThreads, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(),
+                                                                                rank.as<u32>(), rb, k64, hubs);
         G2M_CUDA(cudaGetLastError());
         phase("scan+keys");
         size_t tb2 = 0;

@@ -80,11 +80,56 @@ def test_rmat12_known_counts():
     assert pm.subgraph_listing(g, cycle4(), mode="count").counts["4-cycle"] == 52799071
 
 
+def _hub_graph(scale=12):
+    """R-MAT plus rows longer than the warp row passes take (g2m.cu kHubRow =
+    2048, kRowSortWarp = 1024; at scale 14 also > kRowSortBlock = 8192)."""
+    n = 1 << scale
+    e = [G.rmat_edges(scale, 8, 5)]
+    for hub, k in ((7, n - 1), (9, 3000), (4000, 2049), (11, 2048), (13, 1025), (15, 1024), (17, 33)):
+        others = np.array([v for v in range(k + 1) if v != hub][:k], dtype=np.int64)
+        e.append(np.column_stack([np.full(len(others), hub), others]))
+    return GR.from_edges(np.concatenate(e), num_vertices=n)
+
+
 def test_device_orientation_equals_host():
-    g = GR.from_edges(G.rmat_edges(11, 16, 3), num_vertices=1 << 11)
-    og = GR.orient(g)
-    ho = orient_host(g)
-    assert og == ho and og.max_degree == ho.max_degree and og.oriented
+    for g in (GR.from_edges(G.rmat_edges(11, 16, 3), num_vertices=1 << 11), _hub_graph()):
+        og = GR.orient(g)
+        ho = orient_host(g)
+        assert og == ho and og.max_degree == ho.max_degree and og.oriented
+
+
+def test_hub_rows_rank_build():
+    """Hub rows go through the block-per-row passes of orientation and the
+    rank relabelling; the rank-space kernels must still equal the generated
+    kernels on the original ids."""
+    g = _hub_graph()
+    assert g.max_degree > 4000
+    for gs in (g, _hub_graph(14)):
+        for pat, rw in ((cycle4(), False), (diamond(), True)):
+            f = PL.as_forest(make_plan(pat, gs, rewrite=rw))
+            tasks = EX._default_tasks(gs, f)
+            assert EX.execute(gs, f, tasks, lgs=True)[0] == EX.execute(gs, f, tasks, lgs=False)[0]
+    og = orient_host(g)
+    want = {}
+    for k in (3, 4):
+        f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
+        tasks = EX._default_tasks(og, f)
+        want[k] = EX.execute(og, f, tasks, lgs=False)[0]
+        assert EX.execute(og, f, tasks, lgs=True)[0] == want[k]
+    # public API: device orientation (hub blocks) -> rank build -> LGS
+    assert pm.triangle_count(g) == want[3]["triangle"]
+    assert pm.k_clique(g, 4).counts == want[4]
+
+
+def test_rank_row_sort_equals_radix(monkeypatch):
+    """The per-row rank-space build and the global key sort give the same counts."""
+    g = _hub_graph(14)
+    f = PL.as_forest(make_plan(cycle4(), g))
+    tasks = EX._default_tasks(g, f)
+    a = EX.execute(g, f, tasks)[0]
+    g2 = _hub_graph(14)
+    monkeypatch.setenv("G2M_RANK_RADIX", "1")
+    assert EX.execute(g2, f, tasks)[0] == a
 
 
 def test_device_csr_builder_equals_host():
