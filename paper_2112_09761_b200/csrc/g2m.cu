@@ -851,8 +851,8 @@ k_rank_keys64_hubs(const u64* off, const u32* nbr, const u32* rank, int rb, u64*
 // Row r = rank[v] of the rank-space CSR holds rank[w] for w in N(v), sorted.
 // Rows of <= 32 are sorted in registers (warp bitonic), rows of <= 1024 in a
 // per-warp shared buffer, longer rows by one 1024-thread block per row in
-// shared memory (<= kRowSortBlock), and the few longer still by a segmented
-// radix sort over just those rows.
+// shared memory (<= kRowSortBlock); graphs with longer rows take the global
+// key sort instead.
 constexpr u32 kRowSortWarp = 1024;
 constexpr u32 kRowSortBlock = 8192;
 constexpr int kFillWarps = 8;
@@ -917,21 +917,14 @@ k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* 
 }
 
 __global__ void __launch_bounds__(kHubThreads)
-k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_off, u32* rk_nbr, const u32* hubs,
-                 u32* big) {
+k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_off, u32* rk_nbr, const u32* hubs) {
     __shared__ u32 sb[kRowSortBlock];
     const u32 nh = hubs[0];
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
         const u32 v = hubs[1 + h];
         const u64 b = off[v];
-        const u32 d = (u32)(off[v + 1] - b);
-        const u32 r = rank[v];
-        u32* out = rk_nbr + rk_off[r];
-        if (d > kRowSortBlock) {   // unsorted; sorted by the segmented pass
-            for (u32 i = threadIdx.x; i < d; i += kHubThreads) out[i] = __ldg(rank + __ldg(nbr + b + i));
-            if (threadIdx.x == 0) push_hub(big, r);
-            continue;
-        }
+        const u32 d = (u32)(off[v + 1] - b);   // <= kRowSortBlock (host check)
+        u32* out = rk_nbr + rk_off[rank[v]];
         const u32 P = 1u << (32 - __clz(d - 1));
         for (u32 i = threadIdx.x; i < P; i += kHubThreads) sb[i] = i < d ? __ldg(rank + __ldg(nbr + b + i)) : 0xffffffffu;
         __syncthreads();
@@ -939,19 +932,6 @@ k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_
         for (u32 i = threadIdx.x; i < d; i += kHubThreads) out[i] = sb[i];
         __syncthreads();
     }
-}
-
-__global__ void k_big_segments(const u32* big, const u64* rk_off, u64* beg, u64* end) {
-    const u32 n = big[0];
-    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        beg[i] = rk_off[big[1 + i]];
-        end[i] = rk_off[big[1 + i] + 1];
-    }
-}
-
-__global__ void k_copy_segments(const u32* src, u32* dst, const u64* beg, const u64* end, u32 n) {
-    for (u32 s = blockIdx.x; s < n; s += gridDim.x)
-        for (u64 i = beg[s] + threadIdx.x; i < end[s]; i += blockDim.x) dst[i] = src[i];
 }
 
 __global__ void k_low_bits(const u64* keys, u64 n, int rb, u32* out) {
@@ -1010,49 +990,18 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     }
     phase("keys+sort+scatter");
     G2M_TRY(exclusive_scan_u64(st, rdeg.as<u64>(), g->rk_off.as<u64>(), nv));
-    if (nv && slots && !getenv("G2M_RANK_RADIX")) {
-        // rows written in place and sorted per row
+    // rows of at most kRowSortBlock (oriented graphs; symmetric graphs without
+    // hubs) are written in place and sorted per row; otherwise one global key
+    // sort (a segmented sort leaves a 10^6-slot hub row to one CTA)
+    if (nv && slots && g->maxdeg <= kRowSortBlock && !getenv("G2M_RANK_RADIX")) {
         u32* hubs = nullptr;
         G2M_TRY(hub_list(st, slots, &hubs));
-        DevBuf bigl;
-        G2M_TRY(bigl.ensure((slots / kRowSortBlock + 2) * 4));
-        G2M_CUDA(cudaMemsetAsync(bigl.p, 0, 4, st->stream));
         st->launches += 2;
         k_rank_fill<<<grid_for(st, nv * 32, kFillWarps * 32), kFillWarps * 32, 0, st->stream>>>(
             g->off.as<u64>(), g->nbr.as<u32>(), nv, rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs);
         k_rank_fill_hubs<<<hub_grid(st, slots), kHubThreads, 0, st->stream>>>(
-            g->off.as<u64>(), g->nbr.as<u32>(), rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs,
-            bigl.as<u32>());
+            g->off.as<u64>(), g->nbr.as<u32>(), rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs);
         G2M_CUDA(cudaGetLastError());
-        phase("fill+row sort");
-        u32 nbig = 0;
-        G2M_CUDA(cudaMemcpyAsync(&nbig, bigl.p, 4, cudaMemcpyDeviceToHost, st->stream));
-        G2M_CUDA(cudaStreamSynchronize(st->stream));
-        if (nbig) {
-            DevBuf segs;
-            G2M_TRY(segs.ensure((u64)nbig * 16));
-            u64* beg = segs.as<u64>();
-            u64* end = beg + nbig;
-            ++st->launches;
-            k_big_segments<<<grid_for(st, nbig, 256), 256, 0, st->stream>>>(bigl.as<u32>(), g->rk_off.as<u64>(), beg,
-                                                                           end);
-            G2M_TRY(st->tmp1.ensure(slots * 4));
-            u32* sorted_out = st->tmp1.as<u32>();
-            int rb = 1;
-            while (rb < 32 && ((u64)1 << rb) < nv) ++rb;
-            size_t tb = 0;
-            G2M_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tb, g->rk_nbr.as<u32>(), sorted_out,
-                                                             (int64_t)slots, (int64_t)nbig, beg, end, 0, rb,
-                                                             st->stream));
-            G2M_TRY(st->cub_tmp.ensure(tb));
-            G2M_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(st->cub_tmp.p, tb, g->rk_nbr.as<u32>(), sorted_out,
-                                                             (int64_t)slots, (int64_t)nbig, beg, end, 0, rb,
-                                                             st->stream));
-            ++st->launches;
-            k_copy_segments<<<std::min<u32>(nbig, st->sms * 4), 1024, 0, st->stream>>>(sorted_out, g->rk_nbr.as<u32>(),
-                                                                                      beg, end, nbig);
-            G2M_CUDA(cudaGetLastError());
-        }
     } else if (nv && slots) {
         int rb = 1;
         while (rb < 32 && ((u64)1 << rb) < nv) ++rb;
@@ -1078,7 +1027,7 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
         G2M_CUDA(cudaGetLastError());
     }
     G2M_CUDA(cudaStreamSynchronize(st->stream));
-    phase("radix sort");
+    phase("rows");
     g->has_rank = true;
     return G2M_OK;
 }

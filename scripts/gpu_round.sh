@@ -11,7 +11,7 @@ done
 # ncu: launch list of one cold cl4 step + full capture of its mining kernels
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_cl4_launches.csv \
   python bench.py --workload cl4 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-roofline > /dev/null 2>&1; echo launches rc=$?
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_clique_(warp|cta)" -c 8 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_clique_(warp|cta|pairs)" -c 10 \
   -o gpurun_out/${T}_cl4_full -f python bench.py --workload cl4 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-roofline > /dev/null 2>&1; echo full rc=$?
 # config C5 on one GPU (device-generated R-MAT)
 timeout 1500 python bench.py --workload tc --scale 27 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${T}_bench_tc27.json 2> gpurun_out/${T}_bench_tc27.err; echo tc27 rc=$?
