@@ -256,6 +256,85 @@ k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* 
     if (lane == 0 && acc) g2m_add128(count, acc, 0);
 }
 
+// ---- tier 3, coarse buckets ----------------------------------------------------
+// As k_c4_stage, but the wedge ends are partitioned into 32K-id buckets (a
+// few hundred per v1 instead of r1/1024): the scatter then has few enough
+// open write cursors per block that L2 combines the partial-sector writes
+// instead of evicting them to DRAM. Each bucket is counted by the whole CTA
+// in dense shared counters, cleared by a re-walk (or densely when the
+// bucket is large).
+constexpr u32 kCoarseBits = 15;
+constexpr u32 kCoarseIds = 1u << kCoarseBits;
+
+__host__ __device__ constexpr size_t stage2_smem_bytes(int NW, u32 nbmax) {
+    return (size_t)4 * nbmax + (size_t)4 * kCoarseIds + (size_t)4 * NW * 96;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
+            const u32* __restrict__ lows, u64 nverts, u64* next, u64* count, u32* stage_all, u64 stage_cap,
+            u32 nbmax, u32 lo_x) {
+    extern __shared__ __align__(16) u32 smem_c4[];
+    constexpr u32 NT = NW * 32;
+    u32* H = smem_c4;
+    u32* C = H + nbmax;
+    const u32 lane = g2m_lane();
+    const u32 w = threadIdx.x >> 5;
+    u32* wscr = C + kCoarseIds + w * 96;
+    u32* stage = stage_all + (u64)blockIdx.x * stage_cap;
+    __shared__ u64 s_t;
+    __shared__ u32 s_row, s_row2;
+    for (u32 x = threadIdx.x; x < kCoarseIds; x += NT) C[x] = 0;
+    u64 acc = 0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            s_t = atomicAdd(next, 1ull);
+            s_row = s_row2 = 0;
+        }
+        __syncthreads();
+        const u64 t = s_t;
+        if (t >= nverts) break;
+        const u32 r1 = __ldg(verts + t);
+        const u32 l1 = __ldg(lows + t);
+        const u32* L = nbr + __ldg(off + r1);
+        const u32 nb = (r1 >> kCoarseBits) + 1;
+        for (u32 b = threadIdx.x; b < nb; b += NT) H[b] = 0;
+        __syncthreads();
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row, wscr, [&](u32 x) { atomicAdd(H + (x >> kCoarseBits), 1u); });
+        __syncthreads();
+        if (w == 0) {
+            u32 carry = 0;
+            for (u32 b0 = 0; b0 < nb; b0 += 32) {
+                const u32 b = b0 + lane;
+                const u32 v = b < nb ? H[b] : 0u;
+                const u32 incl = g2m_scan_incl(v);
+                if (b < nb) H[b] = carry + incl - v;
+                carry += __shfl_sync(G2M_FULL, incl, 31);
+            }
+        }
+        __syncthreads();
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row2, wscr, [&](u32 x) {
+            stage[atomicAdd(H + (x >> kCoarseBits), 1u)] = x;
+        });
+        __syncthreads();
+        for (u32 b = 0; b < nb; ++b) {
+            const u32 s0 = b ? H[b - 1] : 0u, s1 = H[b];
+            if (s0 == s1) continue;
+            for (u32 e = s0 + threadIdx.x; e < s1; e += NT) acc += atomicAdd(C + (stage[e] & (kCoarseIds - 1)), 1u);
+            __syncthreads();
+            if (s1 - s0 > kCoarseIds / 4) {
+                for (u32 x = threadIdx.x; x < kCoarseIds; x += NT) C[x] = 0;
+            } else {
+                for (u32 e = s0 + threadIdx.x; e < s1; e += NT) C[stage[e] & (kCoarseIds - 1)] = 0;
+            }
+            __syncthreads();
+        }
+    }
+    acc = g2m_wsum(acc);
+    if (lane == 0 && acc) g2m_add128(count, acc, 0);
+}
+
 // ---- tier 4: the whole grid on one v1, shared dense counters -----------------
 // The v1's wedges are flattened over the grid: k_c4_rows writes each row's
 // wedge count and first nbr index, a scan makes the ends, and k_c4_grid's

@@ -1974,9 +1974,20 @@ extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, c
     G2M_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->dev));
     const u32 nbmax = (u32)((nv >> g2m_c4::kBucketBits) + 2 + 3) & ~3u;   // keeps the u64 scratch aligned
     const size_t stage_smem = g2m_c4::stage_smem_bytes(NW, nbmax);
-    const bool tier3 = stage_smem <= (size_t)max_smem;
+    // coarse-bucket staging (k_c4_stage2, 32 warps) unless G2M_C4_FINE selects the 1024-id buckets
+    // Fine buckets while every block's open write cursors (one 32 B sector per
+    // bucket) fit a quarter of L2 together; beyond that the scatter thrashes
+    // L2 and the coarse buckets win (RMAT-24: 2.63 -> 1.55 s).
+    int l2 = 0;
+    G2M_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->dev));
+    bool coarse = (u64)nbmax * 32 * st->sms > (u64)l2 / 4;
+    if (const char* e = getenv("G2M_C4_FINE")) coarse = atoi(e) == 0;
+    constexpr int NW2 = 32;
+    const u32 nbmax2 = (u32)((nv >> g2m_c4::kCoarseBits) + 2 + 3) & ~3u;
+    const size_t stage2_smem = g2m_c4::stage2_smem_bytes(NW2, nbmax2);
+    const bool tier3 = (coarse ? stage2_smem : stage_smem) <= (size_t)max_smem;
     u64 stage_cap = tier3 ? ((u64)16 << 20) : 0;           // wedges per v1 staged (64 MB per block)
-    if (const char* e = getenv("G2M_C4_STAGE_CAP")) stage_cap = std::min<u64>(stage_cap, strtoull(e, nullptr, 10));
+    if (const char* e = getenv("G2M_C4_STAGE_CAP")) stage_cap = tier3 ? strtoull(e, nullptr, 10) : 0;
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
     G2M_TRY(st->counters.ensure(32 * 8));
     u64* ctr = st->counters.as<u64>();
@@ -2058,7 +2069,23 @@ extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, c
                                                                  sizes[2], next + 1, count, cap, lo_x);
         }));
     }
-    if (sizes[3]) {
+    if (sizes[3] && coarse) {
+        auto kern = g2m_c4::k_c4_stage2<NW2>;
+        G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage2_smem));
+        int occ = 0;
+        G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW2 * 32, stage2_smem));
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        u64 grid = std::min<u64>(sizes[3], (u64)st->sms * std::max(occ, 1));
+        grid = std::min<u64>(grid, std::max<u64>(1, (fr + st->c4slab.bytes) / 4 / (stage_cap * 4)));
+        G2M_TRY(st->c4slab.ensure(grid * stage_cap * 4));
+        G2M_TRY(timed([&] {
+            ++st->launches;
+            kern<<<(unsigned)grid, NW2 * 32, stage2_smem, st->stream>>>(off, nbr, lists + 3 * stride,
+                                                                         lows + 3 * stride, sizes[3], next + 2, count,
+                                                                         st->c4slab.as<u32>(), stage_cap, nbmax2, lo_x);
+        }));
+    } else if (sizes[3]) {
         auto kern = g2m_c4::k_c4_stage<NW>;
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_smem));
         int occ = 0;

@@ -474,6 +474,20 @@ def test_cycle4_grid_tier(monkeypatch):
     assert EX.execute(g, f, tasks)[0] == want
 
 
+@pytest.mark.parametrize("fine", ["0", "1"])
+def test_cycle4_stage_bucket_variants(monkeypatch, fine):
+    """Staged tier with 32K-id coarse buckets (k_c4_stage2) and 1024-id fine
+    buckets (k_c4_stage), with a stage cap that also sends v1s to the grid tier."""
+    g = GR.from_edges(G.rmat_edges(16, 8, 6), num_vertices=1 << 16)   # r1 > 32K: several coarse buckets
+    f = PL.as_forest(make_plan(cycle4(), g))
+    tasks = EX._default_tasks(g, f)
+    want = EX.execute(g, f, tasks, lgs=False)[0]
+    monkeypatch.setenv("G2M_C4_FINE", fine)
+    assert EX.execute(g, f, tasks)[0] == want
+    monkeypatch.setenv("G2M_C4_STAGE_CAP", "100000")
+    assert EX.execute(g, f, tasks)[0] == want
+
+
 def test_diamond_support_kernels_match_generic_and_oracle():
     """g2m_diamond_count (edge triangle support over the rank-space DAG) ==
     the generated diamond plan kernel (counting rewrite) == the oracle."""
