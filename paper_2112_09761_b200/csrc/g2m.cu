@@ -374,61 +374,98 @@ __device__ __forceinline__ u64 block_sum_hub(u64 v, u64* red) {
     return t;
 }
 
-__global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u64 nv, u64* cnt, u32* hubs) {
+// The count pass keeps each 32-slot chunk's keep ballot, so the fill pass
+// compacts without gathering the degree table again. Chunk c of row u
+// (slots b + 32c ..) lives at (b >> 5) + u + c: distinct over all rows,
+// at most slots / 32 + nv + 1 words.
+__device__ __forceinline__ u64 keep_word(u64 b, u64 u, u64 base) { return (b >> 5) + u + ((base - b) >> 5); }
+
+// Light rows in groups of 32: lane j fetches row v0 + j's offsets, then the
+// warp walks the group's rows (one dependent load less per row).
+__global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u64 nv, u64* cnt, u32* hubs,
+                               u32* keep) {
     const u32 lane = g2m_lane();
-    for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
-         u += ((u64)gridDim.x * blockDim.x) >> 5) {
-        const u64 b = off[u], e = off[u + 1];
-        const u32 du = (u32)(e - b);
-        if (du > kHubRow) {
-            if (lane == 0) push_hub(hubs, (u32)u);
-            continue;
+    for (u64 v0 = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; v0 < nv;
+         v0 += (((u64)gridDim.x * blockDim.x) >> 5) * 32) {
+        const u64 vl = v0 + lane;
+        u64 bl = 0, el = 0;
+        if (vl < nv) {
+            bl = off[vl];
+            el = off[vl + 1];
         }
-        u32 c = 0;
-        for (u64 base = b; base < e; base += 32) {
-            const u64 i = base + lane;
-            u32 x = 0;
-            if (i < e) x = __ldg(nbr + i);
-            const bool k = i < e && orient_keep(du, (u32)u, __ldg(deg + x), x);
-            c += __popc(__ballot_sync(G2M_FULL, k));
+        u32 mycnt = 0;
+        const u32 nonempty = __ballot_sync(G2M_FULL, el > bl);
+        for (u32 todo = nonempty; todo; todo &= todo - 1) {
+            const u32 j = __ffs(todo) - 1;
+            const u64 b = __shfl_sync(G2M_FULL, bl, j), e = __shfl_sync(G2M_FULL, el, j);
+            const u32 u = (u32)(v0 + j);
+            const u32 du = (u32)(e - b);
+            if (du > kHubRow) {
+                if (lane == 0) push_hub(hubs, u);
+                continue;
+            }
+            u32 c = 0;
+            for (u64 base = b; base < e; base += 32) {
+                const u64 i = base + lane;
+                u32 x = 0;
+                if (i < e) x = __ldg(nbr + i);
+                const bool k = i < e && orient_keep(du, u, __ldg(deg + x), x);
+                const u32 m = __ballot_sync(G2M_FULL, k);
+                if (lane == 0) keep[keep_word(b, u, base)] = m;
+                c += __popc(m);
+            }
+            if (lane == j) mycnt = c;
         }
-        if (lane == 0) cnt[u] = c;
+        // hub rows are overwritten by k_orient_count_hubs
+        if (vl < nv) cnt[vl] = mycnt;
     }
 }
 
 __global__ void __launch_bounds__(kHubThreads)
-k_orient_count_hubs(const u64* off, const u32* nbr, const u32* deg, const u32* hubs, u64* cnt) {
+k_orient_count_hubs(const u64* off, const u32* nbr, const u32* deg, const u32* hubs, u64* cnt, u32* keep) {
     __shared__ u64 red[kHubThreads / 32];
     const u32 nh = hubs[0];
+    const u32 lane = g2m_lane(), wid = threadIdx.x >> 5;
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
         const u32 u = hubs[1 + h];
         const u64 b = off[u], e = off[u + 1];
         const u32 du = (u32)(e - b);
         u64 c = 0;
-        for (u64 i = b + threadIdx.x; i < e; i += kHubThreads) {
-            const u32 x = __ldg(nbr + i);
-            c += orient_keep(du, u, __ldg(deg + x), x) ? 1 : 0;
+        for (u64 base = b; base < e; base += kHubThreads) {
+            const u64 i = base + threadIdx.x;
+            const u32 x = i < e ? __ldg(nbr + i) : 0u;
+            const bool k = i < e && orient_keep(du, u, __ldg(deg + x), x);
+            const u32 m = __ballot_sync(G2M_FULL, k);
+            if (lane == 0 && base + 32 * wid < e) keep[keep_word(b, u, base + 32 * wid)] = m;
+            c += k ? 1 : 0;
         }
         c = block_sum_hub(c, red);
         if (threadIdx.x == 0) cnt[u] = c;
     }
 }
 
-__global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* deg, u64 nv, const u64* noff, u32* out) {
+__global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* keep, u64 nv, const u64* noff, u32* out) {
     const u32 lane = g2m_lane();
-    for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
-         u += ((u64)gridDim.x * blockDim.x) >> 5) {
-        const u64 b = off[u], e = off[u + 1];
-        const u32 du = (u32)(e - b);
-        if (du > kHubRow) continue;   // k_orient_fill_hubs
-        u64 w = noff[u];
-        for (u64 base = b; base < e; base += 32) {
-            const u64 i = base + lane;
-            const u32 x = i < e ? __ldg(nbr + i) : 0u;
-            const bool k = i < e && orient_keep(du, (u32)u, __ldg(deg + x), x);
-            const u32 m = __ballot_sync(G2M_FULL, k);
-            if (k) out[w + __popc(m & g2m_lanemask_lt())] = x;
-            w += __popc(m);
+    for (u64 v0 = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; v0 < nv;
+         v0 += (((u64)gridDim.x * blockDim.x) >> 5) * 32) {
+        const u64 vl = v0 + lane;
+        u64 bl = 0, el = 0, wl = 0;
+        if (vl < nv) {
+            bl = off[vl];
+            el = off[vl + 1];
+            wl = noff[vl];
+        }
+        const u32 light = __ballot_sync(G2M_FULL, el > bl && el - bl <= kHubRow);   // hubs: k_orient_fill_hubs
+        for (u32 todo = light; todo; todo &= todo - 1) {
+            const u32 j = __ffs(todo) - 1;
+            const u64 b = __shfl_sync(G2M_FULL, bl, j), e = __shfl_sync(G2M_FULL, el, j);
+            u64 w = __shfl_sync(G2M_FULL, wl, j);
+            const u64 u = v0 + j;
+            for (u64 base = b; base < e; base += 32) {
+                const u32 m = __ldg(keep + keep_word(b, u, base));
+                if ((m >> lane) & 1u) out[w + __popc(m & g2m_lanemask_lt())] = __ldg(nbr + base + lane);
+                w += __popc(m);
+            }
         }
     }
 }
@@ -436,20 +473,19 @@ __global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* deg, u6
 // Ordered compaction of a hub row: 1024-slot steps, warp ballots, warp
 // offsets from a shared prefix.
 __global__ void __launch_bounds__(kHubThreads)
-k_orient_fill_hubs(const u64* off, const u32* nbr, const u32* deg, const u32* hubs, const u64* noff, u32* out) {
+k_orient_fill_hubs(const u64* off, const u32* nbr, const u32* keep, const u32* hubs, const u64* noff, u32* out) {
     __shared__ u32 wc[kHubThreads / 32];
     const u32 lane = g2m_lane(), wid = threadIdx.x >> 5;
     const u32 nh = hubs[0];
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
         const u32 u = hubs[1 + h];
         const u64 b = off[u], e = off[u + 1];
-        const u32 du = (u32)(e - b);
         u64 w = noff[u];
         for (u64 base = b; base < e; base += kHubThreads) {
-            const u64 i = base + threadIdx.x;
-            const u32 x = i < e ? __ldg(nbr + i) : 0u;
-            const bool k = i < e && orient_keep(du, u, __ldg(deg + x), x);
-            const u32 m = __ballot_sync(G2M_FULL, k);
+            const u64 wb = base + 32 * wid;
+            const u32 m = wb < e ? __ldg(keep + keep_word(b, u, wb)) : 0u;
+            const bool k = (m >> lane) & 1u;
+            const u32 x = k ? __ldg(nbr + wb + lane) : 0u;
             if (lane == 0) wc[wid] = __popc(m);
             __syncthreads();
             u32 before = 0, tot = 0;
@@ -465,8 +501,9 @@ k_orient_fill_hubs(const u64* off, const u32* nbr, const u32* deg, const u32* hu
     }
 }
 
-static int hub_list(DevState* st, uint64_t slots, u32** out) {
-    G2M_TRY(st->hubs.ensure((slots / kHubRow + 2) * 4));
+// List of the rows longer than min_row: at most slots / (min_row + 1) of them.
+static int hub_list(DevState* st, uint64_t slots, u32 min_row, u32** out) {
+    G2M_TRY(st->hubs.ensure((slots / (min_row + 1) + 2) * 4));
     G2M_CUDA(cudaMemsetAsync(st->hubs.p, 0, 4, st->stream));
     *out = st->hubs.as<u32>();
     return G2M_OK;
@@ -504,18 +541,20 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     DevBuf& cnt = st->tmp1;   // grow-only scratch (the caller holds the device lock)
     DevBuf& deg = st->tmp2;
     u32* hubs = nullptr;
+    DevBuf keep;   // keep ballots of the count pass
+    G2M_TRY(keep.ensure(((g->slots >> 5) + g->nv + 2) * 4));
     G2M_TRY(cnt.ensure(std::max<uint64_t>(g->nv, 1) * 8));
     G2M_TRY(deg.ensure(std::max<uint64_t>(g->nv, 1) * 4));
     if (g->nv) {
         ++st->launches;
         k_degrees<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, deg.as<u32>());
         int grid = grid_for(st, g->nv * 32, 256);
-        G2M_TRY(hub_list(st, g->slots, &hubs));
+        G2M_TRY(hub_list(st, g->slots, kHubRow, &hubs));
         st->launches += 2;
         k_orient_count<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv,
-                                                      cnt.as<u64>(), hubs);
+                                                      cnt.as<u64>(), hubs, keep.as<u32>());
         k_orient_count_hubs<<<hub_grid(st, g->slots), kHubThreads, 0, st->stream>>>(
-            g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), hubs, cnt.as<u64>());
+            g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), hubs, cnt.as<u64>(), keep.as<u32>());
         G2M_CUDA(cudaGetLastError());
     }
     phase("degrees+count");
@@ -527,10 +566,10 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     if (g->nv) {
         int grid = grid_for(st, g->nv * 32, 256);
         st->launches += 2;
-        k_orient_fill<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv,
+        k_orient_fill<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), keep.as<u32>(), g->nv,
                                                      o->off.as<u64>(), o->nbr.as<u32>());
         k_orient_fill_hubs<<<hub_grid(st, g->slots), kHubThreads, 0, st->stream>>>(
-            g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), hubs, o->off.as<u64>(), o->nbr.as<u32>());
+            g->off.as<u64>(), g->nbr.as<u32>(), keep.as<u32>(), hubs, o->off.as<u64>(), o->nbr.as<u32>());
         G2M_CUDA(cudaGetLastError());
     }
     if (g->labels.p) {
@@ -891,28 +930,40 @@ k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* 
     __shared__ u32 buf[kFillWarps][kRowSortWarp];
     const u32 lane = g2m_lane();
     u32* sb = buf[threadIdx.x >> 5];
-    for (u64 v = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; v < nv;
-         v += ((u64)gridDim.x * blockDim.x) >> 5) {
-        const u64 b = off[v], e = off[v + 1];
-        const u32 d = (u32)(e - b);
-        if (d == 0) continue;
-        if (d > kRowSortWarp) {
-            if (lane == 0) push_hub(hubs, (u32)v);
-            continue;
+    // rows in groups of 32: each lane fetches one row's offsets and its
+    // rank-space destination, so the per-row chain is nbr -> rank only
+    for (u64 v0 = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; v0 < nv;
+         v0 += (((u64)gridDim.x * blockDim.x) >> 5) * 32) {
+        const u64 vl = v0 + lane;
+        u64 bl = 0, dl = 0, ol = 0;
+        if (vl < nv) {
+            bl = off[vl];
+            dl = off[vl + 1] - bl;
+            if (dl) ol = rk_off[rank[vl]];
         }
-        u32* out = rk_nbr + rk_off[rank[v]];
-        if (d <= 32) {
-            u32 x = lane < d ? __ldg(rank + __ldg(nbr + b + lane)) : 0xffffffffu;
-            x = bitonic32(x, lane);
-            if (lane < d) out[lane] = x;
-            continue;
+        const u32 nonempty = __ballot_sync(G2M_FULL, dl != 0);
+        for (u32 todo = nonempty; todo; todo &= todo - 1) {
+            const u32 j = __ffs(todo) - 1;
+            const u64 b = __shfl_sync(G2M_FULL, bl, j);
+            const u32 d = (u32)__shfl_sync(G2M_FULL, dl, j);
+            u32* out = rk_nbr + __shfl_sync(G2M_FULL, ol, j);
+            if (d > kRowSortWarp) {
+                if (lane == 0) push_hub(hubs, (u32)(v0 + j));
+                continue;
+            }
+            if (d <= 32) {
+                u32 x = lane < d ? __ldg(rank + __ldg(nbr + b + lane)) : 0xffffffffu;
+                x = bitonic32(x, lane);
+                if (lane < d) out[lane] = x;
+                continue;
+            }
+            const u32 P = 1u << (32 - __clz(d - 1));
+            for (u32 i = lane; i < P; i += 32) sb[i] = i < d ? __ldg(rank + __ldg(nbr + b + i)) : 0xffffffffu;
+            __syncwarp();
+            bitonic_smem(sb, P, lane, 32, [] { __syncwarp(); });
+            for (u32 i = lane; i < d; i += 32) out[i] = sb[i];
+            __syncwarp();
         }
-        const u32 P = 1u << (32 - __clz(d - 1));
-        for (u32 i = lane; i < P; i += 32) sb[i] = i < d ? __ldg(rank + __ldg(nbr + b + i)) : 0xffffffffu;
-        __syncwarp();
-        bitonic_smem(sb, P, lane, 32, [] { __syncwarp(); });
-        for (u32 i = lane; i < d; i += 32) out[i] = sb[i];
-        __syncwarp();
     }
 }
 
@@ -995,7 +1046,7 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     // sort (a segmented sort leaves a 10^6-slot hub row to one CTA)
     if (nv && slots && g->maxdeg <= kRowSortBlock && !getenv("G2M_RANK_RADIX")) {
         u32* hubs = nullptr;
-        G2M_TRY(hub_list(st, slots, &hubs));
+        G2M_TRY(hub_list(st, slots, kRowSortWarp, &hubs));
         st->launches += 2;
         k_rank_fill<<<grid_for(st, nv * 32, kFillWarps * 32), kFillWarps * 32, 0, st->stream>>>(
             g->off.as<u64>(), g->nbr.as<u32>(), nv, rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs);
@@ -1010,7 +1061,7 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
         u64* k64 = st->tmp1.as<u64>();
         u64* s64 = st->tmp2.as<u64>();
         u32* hubs = nullptr;
-        G2M_TRY(hub_list(st, slots, &hubs));
+        G2M_TRY(hub_list(st, slots, kHubRow, &hubs));
         st->launches += 2;
         k_rank_keys64<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), nv,
                                                                             rank.as<u32>(), rb, k64, hubs);

@@ -121,6 +121,14 @@ def test_hub_rows_rank_build():
     assert pm.k_clique(g, 4).counts == want[4]
 
 
+def test_rank_build_many_block_rows():
+    """K_1100: every row (1,099 slots) takes the block row sort, more rows than
+    slots / 2048 (hub-list capacity per row threshold)."""
+    g = complete(1100)
+    assert pm.subgraph_listing(g, cycle4(), mode="count").counts["4-cycle"] == 3 * comb(1100, 4)
+    assert pm.triangle_count(g) == comb(1100, 3)
+
+
 def test_rank_row_sort_equals_radix(monkeypatch):
     """The per-row rank-space build and the global key sort give the same counts."""
     g = _hub_graph(12)   # rows up to 4095: warp and block row sorts
