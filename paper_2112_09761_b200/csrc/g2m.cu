@@ -1774,17 +1774,26 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     return G2M_OK;
 }
 
+static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part, const g2m_kernel* fallback,
+                       const g2m_run_config* cfg, uint64_t* counts, g2m_run_stats* stats, DevState* st);
+
 extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
                                 const g2m_kernel* fallback, const g2m_run_config* cfg,
                                 uint64_t* counts, g2m_run_stats* stats) {
     if (!g || !counts) return fail(G2M_EUSAGE, "null argument");
     if (!g->oriented) return fail(G2M_EUSAGE, "plan orientation does not match the graph");
     if (k < 3 || k > 5) return fail(G2M_EUSAGE, "bitmap clique kernels cover 3 <= k <= 5");
-    auto t0 = Clock::now();
     DevState* st;
     G2M_TRY(dev_state(g->dev, &st));
     std::lock_guard<std::mutex> lk(st->mu);
     G2M_CUDA(cudaSetDevice(g->dev));
+    return clique_impl(g, k, part, fallback, cfg, counts, stats, st);
+}
+
+// g2m_clique_count with the device lock held
+static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part, const g2m_kernel* fallback,
+                       const g2m_run_config* cfg, uint64_t* counts, g2m_run_stats* stats, DevState* st) {
+    auto t0 = Clock::now();
     g2m_run_stats local{};
     g2m_run_stats* S = stats ? stats : &local;
     std::memset(S, 0, sizeof(*S));
@@ -1991,16 +2000,25 @@ extern "C" int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, 
 // 4-cycle count by wedge aggregation (cycle4_kernels.cuh)
 // ---------------------------------------------------------------------------
 
+static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* counts, g2m_run_stats* stats,
+                       DevState* st);
+
 extern "C" int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, const g2m_run_config* cfg,
                                 uint64_t* counts, g2m_run_stats* stats) {
     (void)cfg;
     if (!g || !counts) return fail(G2M_EUSAGE, "null argument");
     if (g->oriented) return fail(G2M_EUSAGE, "plan orientation does not match the graph");
-    auto t0 = Clock::now();
     DevState* st;
     G2M_TRY(dev_state(g->dev, &st));
     std::lock_guard<std::mutex> lk(st->mu);
     G2M_CUDA(cudaSetDevice(g->dev));
+    return cycle4_impl(g, part, counts, stats, st);
+}
+
+// g2m_cycle4_count with the device lock held
+static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* counts, g2m_run_stats* stats,
+                       DevState* st) {
+    auto t0 = Clock::now();
     g2m_run_stats local{};
     g2m_run_stats* S = stats ? stats : &local;
     std::memset(S, 0, sizeof(*S));
