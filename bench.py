@@ -10,17 +10,32 @@ configs are workloads of the same line format:
                     [--scale S] [--n N] [--impl b200|reference]
 
     tc, cl4, cl5   k-clique count, RMAT-22 (configs[1]; TC also configs[4])
-    c4, diamond    subgraph listing count, RMAT-24 (configs[2])
+    c4, diamond    subgraph listing count, RMAT-24 (configs[2]; 4-cycle also configs[4])
     mc3, mc4       k-motif count, power-law n=200,000 m=4 seed 3 (configs[3])
 
-A step is one complete count pass over the whole (N>1: this rank's chunked
-round-robin share of the) task list with the (oriented) graph resident in
-HBM, i.e. what ``run_job`` executes after its host-side decisions
-(apps.prepare_job). ``value`` = E / step time (undirected input edges per
-second, whole job; time = max over ranks of the device step time). ``e2e``
-runs the same count through the public API (``pm.k_clique``,
-``pm.subgraph_listing``, ``pm.k_motif``) from pinned host CSR buffers every
-step: H2D of the CSR, device orientation, the kernels, D2H of the counts.
+A step is one complete count pass over the whole (N>1: this rank's share of
+the) task list with the (oriented) graph resident in HBM, i.e. what
+``run_job`` executes after its host-side decisions (apps.prepare_job).
+``value`` = E / step time (undirected input edges per second, whole job;
+time = max over ranks of the device step time). ``e2e`` runs the same count
+through the public API (``pm.k_clique``, ``pm.subgraph_listing``,
+``pm.k_motif``) from pinned host CSR buffers every step: H2D of the CSR,
+device orientation, the kernels, D2H of the counts.
+
+``--gpus N`` with N > 1 outside torchrun re-launches this script under
+``torch.distributed.run`` with N ranks (one per GPU, NCCL; with
+G2M_BENCH_BACKEND=gloo the ranks fold onto the visible GPUs). Each rank mines
+its share: edge tasks by chunked round-robin with c = 2 * resident warps,
+sources of the bitmap-LGS / wedge kernels by the workload estimator
+(executor.source_spec). The line carries every rank's kernel time and the
+max/mean imbalance.
+
+``parity`` (every line) checks the step's count at full scale two ways:
+the specialised kernels against the generated plan kernel (over every task,
+or over the same residue class of rank-space sources), and the plan kernel
+against the CPU oracle on a seeded task sample (counts are additive over
+tasks, executor.py:84-90).
+
 ``--impl reference`` times the CPU oracle (oracle/oracle.c, the restatement
 of the reference executor) with all host threads on a bounded task sample.
 """
@@ -29,6 +44,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -61,6 +77,16 @@ def peaks():
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
     except Exception:
         return {}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -183,40 +209,154 @@ def api_call(workload, g):
     return {p.name: c for p, c in pm.k_motif(g, arg).items()}
 
 
-def cpu_sample_run(gd, forest, tasks, target_s: float, threads: int, seed: int = 7):
-    """Oracle on a seeded uniform sample of the task list; returns
-    (seconds, sampled tasks, total tasks, counts)."""
-    from oracle import oracle as O
+def sample_tasks(gd, tasks, m: int, seed: int):
+    """A seeded uniform sample of m tasks of the (implicit) task list:
+    (positions in the list, the tasks as the oracle takes them, edge?)."""
     from paper_2112_09761_b200.graph import EdgeTaskList
     off = np.asarray(gd.row_offsets, dtype=np.int64)
     nbr = gd.neighbors
     edge = isinstance(tasks, EdgeTaskList)
-    slots = None
     if edge and tasks.reduced:
-        src_all = np.repeat(np.arange(gd.num_vertices, dtype=np.int64), np.diff(off))
-        slots = np.flatnonzero(nbr.astype(np.int64) < src_all)
-        del src_all
+        # position p of the reduced list = the p-th slot with dst < src
+        lower = np.empty(len(nbr), dtype=bool)
+        nv = gd.num_vertices
+        step = 1 << 20
+        for r0 in range(0, nv, step):
+            r1 = min(nv, r0 + step)
+            s0, s1 = int(off[r0]), int(off[r1])
+            src = np.repeat(np.arange(r0, r1, dtype=np.uint32), np.diff(off[r0:r1 + 1]))
+            lower[s0:s1] = nbr[s0:s1] < src
+        slots = np.flatnonzero(lower)
+        del lower
+    else:
+        slots = None
     total = len(slots) if slots is not None else (int(off[-1]) if edge else gd.num_vertices)
     rng = np.random.default_rng(seed)
+    pick = np.sort(rng.choice(total, size=min(m, total), replace=False)).astype(np.int64)
+    if not edge:
+        return pick, pick, False, total
+    s = slots[pick] if slots is not None else pick
+    src = np.searchsorted(off, s, side="right") - 1
+    return pick, np.column_stack([src, nbr[s].astype(np.int64)]), True, total
 
-    def sample(m):
-        pick = rng.choice(total, size=min(m, total), replace=False)
-        pick.sort()
-        if not edge:
-            return pick.astype(np.int64)
-        s = slots[pick] if slots is not None else pick
-        src = np.searchsorted(off, s, side="right") - 1
-        return np.column_stack([src, nbr[s].astype(np.int64)])
 
+def cpu_sample_run(gd, forest, tasks, target_s: float, threads: int, seed: int = 7):
+    """Oracle on a seeded uniform sample of the task list; returns
+    (seconds, sampled tasks, total tasks, counts, sample positions)."""
+    from oracle import oracle as O
     m = 2000
     while True:
-        tk = sample(m)
+        pick, tk, edge, total = sample_tasks(gd, tasks, m, seed)
         t0 = time.perf_counter()
         counts, _ = O.run(gd, forest, tasks=tk, edge=edge, threads=threads)
         dt = time.perf_counter() - t0
         if dt >= target_s * 0.5 or m >= total:
-            return dt, len(tk), total, counts
+            return dt, len(tk), total, counts, pick
         m = int(min(total, m * max(2.0, 0.8 * target_s / max(dt, 1e-3))))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args_n: int) -> int:
+    """--gpus N outside torchrun: run this script under torch.distributed.run
+    with N ranks on this node and pass rank 0's line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args_n}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    log("relaunching under torchrun:", " ".join(cmd[2:6]), "...")
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------------------
+# roofline: the specialised kernels' own algorithmic bytes
+# ---------------------------------------------------------------------------
+
+def kernel_operands(family: str, gd, forest, tasks, local, rank, args):
+    """(operand bytes per step, how, units) of the kernels the step runs.
+    lgs / cycle4 / diamond: the specialised algorithm's compulsory operand
+    reads (g2m_kernel_work); plan: the instrumented plan kernel's SURVEY
+    8(d) bytes (its algorithm is the reference plan)."""
+    from paper_2112_09761_b200 import executor as EX
+    from paper_2112_09761_b200 import graph as GR
+    if family == "lgs":
+        ob, probes, _, src = gd.device_graph(local).kernel_work(0)
+        return ob, ("bitmap LGS: per source u its offsets + N+(u), per v in N+(u) its offsets + "
+                    "N+(v) (local-graph probes): 16n + 20m + 4 sum_v d-(v)d+(v)"), \
+            {"probed_ids": probes, "sources": src}
+    if family == "cycle4":
+        ob, wedges, upd, src = gd.device_graph(local).kernel_work(1)
+        return ob + 8 * upd, ("wedge aggregation: per top vertex r its offsets + N<(r), per v its "
+                              "offsets + the wedge ends N(v) & [lo_x, r) (4 B each), plus one 4 B "
+                              "counter read-modify-write per wedge (8 B)"), \
+            {"wedges": wedges, "sources": src}
+    if family == "diamond":
+        og = GR.orient(gd, device=local)
+        ob, probes, _, src = og.device_graph(local).kernel_work(0)
+        # + one support counter RMW per triangle edge (3 per triangle found) and
+        # the final pass over the support array
+        return ob + 8 * og.num_edges, ("edge triangle support on the degree-oriented DAG: the "
+                                       "bitmap-LGS operand bytes + a support counter per DAG edge "
+                                       "(read+write)"), {"probed_ids": probes, "sources": src}
+    return None, None, None
+
+
+def binding_from_profiles(workload: str, graph: str):
+    """ncu evidence (profiles/ncu_summary.json, written from a committed
+    `ncu --set full` capture): per-step DRAM bytes and the dominant kernel's
+    utilisation of the resources that bind it."""
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if not f.exists():
+        return None
+    return json.loads(f.read_text()).get(f"{workload}@{graph}")
+
+
+# ---------------------------------------------------------------------------
+# parity at full scale
+# ---------------------------------------------------------------------------
+
+def residue_parity(family, gd, forest, local, counts, P: int, i: int):
+    """Specialised kernels vs the generated plan kernel on the same source
+    set: the rank-space sources r = i (mod P). Both sides work on the rank
+    relabelling (relabelling it again is the identity), the plan kernel over
+    the edge tasks whose first vertex is such an r (the reference plans bind
+    the clique's DAG source / the 4-cycle's largest vertex at v1)."""
+    from paper_2112_09761_b200 import executor as EX
+    from paper_2112_09761_b200 import graph as GR
+    pid = forest.pattern_ids[0]
+    spec_c, _, _, _ = EX.execute(gd, forest, EX._default_tasks(gd, forest), device=local,
+                                 rr=(1, P, i), source_split=("rr", 1))
+    rg = GR.rank_relabel(gd, device=local)
+    off = np.asarray(rg.row_offsets, dtype=np.int64)
+    rows = np.arange(i, rg.num_vertices, P, dtype=np.int64)
+    if family == "lgs":
+        b, e = off[rows], off[rows + 1]
+        lens = e - b
+        idx = np.repeat(b - np.cumsum(np.concatenate([[0], lens[:-1]])), lens) + np.arange(lens.sum())
+        tasks = EX._default_tasks(rg, forest)
+        plan_c, _, _, _ = EX.execute(rg, forest, tasks, device=local, index=idx.astype(np.int64),
+                                     lgs=False)
+    else:   # 4-cycle: reduced edge tasks (r, w), w < r
+        from paper_2112_09761_b200.graph import EdgeTaskList
+        nbr = rg.neighbors
+        pairs = []
+        for r in rows:
+            seg = nbr[off[r]:off[r + 1]]
+            seg = seg[seg < r]
+            if len(seg):
+                pairs.append(np.column_stack([np.full(len(seg), r, dtype=np.int64),
+                                              seg.astype(np.int64)]))
+        pairs = np.concatenate(pairs) if pairs else np.empty((0, 2), dtype=np.int64)
+        plan_c, _, _, _ = EX.execute(rg, forest, EdgeTaskList(pairs, reduced=True), device=local,
+                                     lgs=False)
+    del rg
+    return {"check": f"specialised kernels vs generated plan kernel on rank-space sources "
+                     f"r = {i} (mod {P})",
+            "specialised": int(spec_c[pid]), "plan_kernel": int(plan_c[pid]),
+            "equal": int(spec_c[pid]) == int(plan_c[pid])}
 
 
 def main():
@@ -233,11 +373,23 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--balg-sample", type=float, default=None,
-                    help="fraction of tasks for the algorithmic-byte count (default: all; 1e-3 for 4-cycle)")
+                    help="fraction of tasks for the reference-equivalent bytes (default: all; "
+                         "1e-3 for 4-cycle)")
+    ap.add_argument("--residue", type=int, default=None,
+                    help="P of the residue-class parity check (default per workload)")
+    ap.add_argument("--simulate-parts", type=int, default=0,
+                    help="1 GPU: run each of P parts of the multi-GPU split in turn and report "
+                         "per-part kernel time and max/mean imbalance")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
+        sys.exit(2)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
@@ -281,23 +433,25 @@ def main():
     gname = (f"RMAT-{spec[1]} (ef16, Graph500 a=.57 b=c=.19, seed 1"
              + (", device RNG)" if build_info.get("generator") else ")") if spec[0] == "rmat"
              else f"power-law n={spec[1]} m=4 seed 3 (cli.gen_synthetic)")
+    graph_key = f"{spec[0]}{spec[1]}"
     config = {"workload": f"{desc} on {gname}", "patterns": list(forest.pattern_ids),
-              "graph": f"{spec[0]}{spec[1]}", "num_vertices": g.num_vertices,
+              "graph": graph_key, "num_vertices": g.num_vertices,
               "undirected_edges": E, "oriented": gd.oriented, "max_degree_task_graph": gd.max_degree,
               "granularity": pj.granularity, "tasks": len(tasks),
               "search": next((d.render() for d in pj.log if d.name == "bounded-bfs"), "dfs"),
-              "parallelism": f"{world} GPU(s), chunked round-robin tasks, graph replicated"
-              if world > 1 else "1 GPU",
+              "parallelism": f"{world} GPU(s): graph replicated, edge tasks by chunked round-robin "
+                             f"(c = 2 x resident warps), LGS/wedge sources by the workload estimator "
+                             f"({EX.SOURCE_SPLIT}:{EX.SOURCE_CHUNK})" if world > 1 else "1 GPU",
               "l2": "inputs larger than L2 (CSR > 126 MB); no flush needed" if gd.num_edges * 4 > 126e6
               else "graph fits L2: measured warm (no flush)"}
     metric = "edges/s"
+    threads = os.cpu_count() or 1
 
     if args.impl == "reference":
-        threads = os.cpu_count() or 1
         steps = []
         for i in range(args.warmup + args.steps):
-            dt, m, total, _ = cpu_sample_run(gd, forest, tasks, args.cpu_seconds / 4, threads,
-                                             seed=100 + i)
+            dt, m, total, _, _ = cpu_sample_run(gd, forest, tasks, args.cpu_seconds / 4, threads,
+                                                seed=100 + i)
             if i >= args.warmup:
                 steps.append(dt * total / m)
         t = float(np.mean(steps))
@@ -308,6 +462,7 @@ def main():
                 "vs_baseline": None, "dtype": "u32 ids / u64 counts", "data": "synthetic",
                 "config": config,
                 "cpu_baseline": {"value": v, "unit": "edges/s", "cores": threads, "kind": "port",
+                                 "cpu_model": cpu_model(),
                                  "sample": f"seeded uniform task sample per step (~{args.cpu_seconds / 4:.0f}s), "
                                            f"extrapolated to all {total} tasks"},
                 "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -315,7 +470,8 @@ def main():
         return
 
     # ------------------------------------------------------------------ b200
-    rr = D.shard(rank, world)
+    rr = D.shard(rank, world, device=local)
+    family = EX.kernel_family(gd, forest, tasks, rr=rr)
 
     def step():   # run_job's search choice (DFS / bounded-frontier BFS), logged as "bounded-bfs"
         counts, st, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, search="auto")
@@ -339,13 +495,23 @@ def main():
     wall = time.perf_counter() - t0
     clocks = sampler.stop()
     my_ms = float(np.mean(dev_ms))
+    my_kms = float(np.mean(kern_ms))
     total_counts = counts
+    per_rank = [{"rank": rank, "device_ms": my_ms, "kernel_ms": my_kms, "tasks": int(st.tasks),
+                 "count": int(sum(counts.values()))}]
     if dist is not None:   # the job's time is its slowest rank; counts add up exactly
         ms = D.allreduce_max(my_ms, device=coll_dev)
         total_counts = D.allreduce_counts(counts, device=coll_dev)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, per_rank[0])
+        per_rank = gathered
     else:
         ms = my_ms
     value = E / (ms / 1000.0)
+    kms_all = [r["kernel_ms"] for r in per_rank]
+    balance = {"per_rank": per_rank,
+               "imbalance_max_over_mean": (max(kms_all) / (sum(kms_all) / len(kms_all)))
+               if sum(kms_all) > 0 else None}
 
     # e2e through the public API from pinned host buffers (N=1), or the
     # upload/orient/run chain per rank (N>1)
@@ -378,18 +544,18 @@ def main():
 
     pk = peaks()
     hbm = pk.get("hbm_gbs") or 6650.0
-    kms = float(np.mean(kern_ms))
-    # SURVEY 8(d) algorithmic bytes of the reference plan over this rank's
-    # tasks, from the instrumented generated kernel (run once, untimed)
-    balg, balg_how = None, None
+    kms = max(kms_all)
+    # --- reference-equivalent bytes (SURVEY 8(d) B_alg) from the instrumented
+    # plan kernel (untimed); also the full-task plan-kernel count for parity
+    balg, balg_how, plan_full = None, None, None
     if not args.no_roofline:
         t_b = time.perf_counter()
         frac = args.balg_sample
-        if frac is None and kind == "sl" and WORKLOADS[args.workload][1] == "4-cycle" and E > 10 ** 7:
+        if frac is None and kind == "sl" and warg == "4-cycle" and E > 10 ** 7:
             frac = 1e-3     # the reference 4-cycle plan is quadratic in hub degree: sample it
+        if frac is None and kind == "clique" and (warg == 5 or E > 2 * 10 ** 8):
+            frac = 1e-2     # 5-clique / RMAT-27: the plan kernel over every task takes minutes
         if frac:
-            # seeded uniform sample of the whole job's tasks through the
-            # instrumented plan kernel, scaled up (rank 0 only)
             balg = 0
             if rank == 0:
                 ntask = len(tasks)
@@ -399,42 +565,118 @@ def main():
                 balg = int(int(bst.alg_bytes) * ntask / len(idx))
                 balg_how = f"sampled: {len(idx)} of {ntask} tasks (seeded uniform), scaled"
         else:
-            _, bst, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, instrument=True)
+            pc, bst, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, instrument=True)
             balg = int(bst.alg_bytes)
             balg_how = "exact: instrumented plan kernel over every task"
-        if dist is not None:   # whole job: bytes add up over ranks, time is the slowest rank's
+            plan_full = pc
+            if dist is not None:
+                plan_full = D.allreduce_counts(pc, device=coll_dev)
+        if dist is not None:   # whole job: bytes add up over ranks
             balg = D.allreduce_counts({"b": balg}, device=coll_dev)["b"]
-            kms = D.allreduce_max(kms, device=coll_dev)
-        log("algorithmic bytes", balg, balg_how, "in", round(time.perf_counter() - t_b, 2), "s")
-    traffic = None
-    tfile = ROOT / "profiles" / "ncu_traffic.json"
-    if tfile.exists() and world == 1:
-        traffic = json.loads(tfile.read_text()).get(f"{args.workload}@{config['graph']}")
-    achieved = balg / (kms / 1000.0) / 1e9 if balg else None
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm if achieved else None,
-            "traffic": traffic.get("dram_bytes_per_step") if traffic else None,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if pk.get("hbm_gbs")
-            else "fallback 6650 (B200_PROFILING.md)",
-            "algorithmic_bytes_per_step": balg,
-            "algorithmic_bytes_how": balg_how,
-            "algorithmic_bytes_def": "SURVEY 8(d): 4B x (|A|+|B|) per reference set op + 4B per "
-                                     "DESCEND candidate + 16B per list opened + 8B/4B per edge/vertex task",
-            "kernel": "mining kernels of one step" + (" (bitmap LGS tiers)" if kind == "clique"
-                                                      else " (generated plan kernel)"),
-            "kernel_ms_per_step": kms,
-            "kernel_share": kms / my_ms if my_ms else None,
-            "physical_dram_frac": (traffic["dram_bytes_per_step"] / (kms / 1000.0) / 1e9 / hbm)
-            if traffic else None,
-            "traffic_source": traffic.get("source") if traffic else None}
+        log("reference-equivalent bytes", balg, balg_how, "in", round(time.perf_counter() - t_b, 2), "s")
 
+    roof = None
+    if not args.no_roofline:
+        ob, ob_how, units = kernel_operands(family, gd, forest, tasks, local, rank, args)
+        if ob is None:      # the generated plan kernel: its own algorithm is the reference plan
+            ob, ob_how, units = balg, "generated plan kernel = the reference plan: " + str(balg_how), None
+        achieved = ob / (kms / 1000.0) / 1e9 if ob else None
+        prof = binding_from_profiles(args.workload, graph_key) if world == 1 else None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm if achieved else None,
+                "traffic": prof.get("dram_bytes_per_step") if prof else None,
+                "peak_source": "of measured: MEASURED_PEAKS.json hbm_gbs (copy)" if pk.get("hbm_gbs")
+                else "of fallback 6650 (B200_PROFILING.md)",
+                "algorithmic_bytes_per_step": ob,
+                "algorithmic_bytes_def": ob_how,
+                "algorithmic_units": units,
+                "kernel": {"lgs": "bitmap local-graph clique tiers (concurrent streams)",
+                           "cycle4": "4-cycle wedge-aggregation tiers",
+                           "diamond": "edge triangle-support tiers + sum C(t,2)",
+                           "plan": "generated plan kernel (DFS or bounded BFS)"}[family],
+                "kernel_ms_per_step": kms,
+                "kernel_share": kms / ms if ms else None,
+                "binding": prof.get("binding") if prof else None,
+                "physical_dram_frac": (prof["dram_bytes_per_step"] / (kms / 1000.0) / 1e9 / hbm)
+                if prof and prof.get("dram_bytes_per_step") else None,
+                "ncu_source": prof.get("source") if prof else None,
+                "reference_equivalent_bytes_per_step": balg,
+                "reference_equivalent_gbs": balg / (kms / 1000.0) / 1e9 if balg else None,
+                "reference_equivalent_how": balg_how}
+
+    # --- parity at full scale
+    parity = None
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        dt, m, total, _ = cpu_sample_run(gd, forest, tasks, args.cpu_seconds, threads)
+    if not args.no_parity:
+        parity = {}
+        pid_counts = {k: int(v) for k, v in total_counts.items()}
+        if plan_full is not None:
+            parity["full_vs_plan_kernel"] = {
+                "check": "step count vs the generated plan kernel over every task",
+                "plan_kernel": {k: int(v) for k, v in plan_full.items()},
+                "equal": {k: int(v) for k, v in plan_full.items()} == pid_counts}
+        elif family in ("lgs", "cycle4") and rank == 0 and world == 1:
+            P = args.residue or (4001 if family == "cycle4" else 101)
+            # the class whose top member is rank nv - P: it skips the P - 1 highest
+            # ranks, the hubs whose 4-cycle plan-kernel work is quadratic in degree
+            i = (gd.num_vertices % P) if family == "cycle4" else 7 % P
+            parity["full_vs_plan_kernel"] = residue_parity(family, gd, forest, local, counts, P, i)
+        elif family in ("diamond",) and world == 1:
+            pc, _, _, _ = EX.execute(gd, forest, tasks, device=local, lgs=False)
+            parity["full_vs_plan_kernel"] = {
+                "check": "step count vs the generated plan kernel over every task",
+                "plan_kernel": {k: int(v) for k, v in pc.items()},
+                "equal": {k: int(v) for k, v in pc.items()} == pid_counts}
+        elif family == "plan" and world == 1:
+            # the step may run bounded BFS or the edge form of a vertex forest;
+            # an explicit index over every task pins plain DFS at the plan's
+            # own granularity
+            pc, _, _, _ = EX.execute(gd, forest, tasks, device=local,
+                                     index=np.arange(len(tasks), dtype=np.int64), lgs=False)
+            parity["full_vs_plan_kernel"] = {
+                "check": "step count (search chosen by run_job) vs plain DFS of the plan kernel "
+                         "over every task at the plan's granularity",
+                "plan_kernel": {k: int(v) for k, v in pc.items()},
+                "equal": {k: int(v) for k, v in pc.items()} == pid_counts}
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline and args.no_parity):
+        dt, m, total, ocounts, pick = cpu_sample_run(gd, forest, tasks, args.cpu_seconds, threads)
         tcpu = dt * total / m
-        cpu = {"value": E / tcpu, "unit": "edges/s", "cores": threads, "kind": "port",
-               "sample": f"{m} of {total} tasks (seeded uniform), {dt:.1f}s, extrapolated"}
+        if not args.no_cpu_baseline:
+            cpu = {"value": E / tcpu, "unit": "edges/s", "cores": threads, "kind": "port",
+                   "cpu_model": cpu_model(),
+                   "sample": f"{m} of {total} tasks (seeded uniform), {dt:.1f}s, extrapolated"}
+        if parity is not None:
+            gc, _, _, _ = EX.execute(gd, forest, tasks, device=local, index=pick, lgs=False)
+            parity["sample_vs_oracle"] = {
+                "check": "generated plan kernel vs the CPU oracle on the same seeded task sample",
+                "sample_tasks": int(m), "of_tasks": int(total),
+                "oracle": {k: int(v) for k, v in ocounts.items()},
+                "plan_kernel": {k: int(v) for k, v in gc.items()},
+                "equal": {k: int(v) for k, v in gc.items()} == {k: int(v) for k, v in ocounts.items()}}
+    if parity is not None:
+        oks = [v["equal"] for v in parity.values()]
+        parity["all_equal"] = bool(oks) and all(oks)
+
+    # --- multi-GPU split simulated on one GPU: each part in turn
+    sim = None
+    if args.simulate_parts > 1 and world == 1:
+        sim = {}
+        P = args.simulate_parts
+        splits = [("est", EX.SOURCE_CHUNK), ("rr", 1)] if family in ("lgs", "cycle4") else [(None, None)]
+        for split, chunk in splits:
+            part_ms, tot = [], {}
+            for i in range(P):
+                rr_i = D.shard(i, P, device=local)
+                c, st_i, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr_i, search="auto",
+                                           source_split=(split, chunk) if split else None)
+                part_ms.append(float(st_i.kernel_ms))
+                for k, v in c.items():
+                    tot[k] = tot.get(k, 0) + int(v)
+            key = f"{split}:{chunk}" if split else "chunked_rr"
+            sim[key] = {"parts": P, "kernel_ms": part_ms,
+                        "imbalance_max_over_mean": max(part_ms) / (sum(part_ms) / P) if sum(part_ms) else None,
+                        "counts_equal_whole": tot == {k: int(v) for k, v in total_counts.items()}}
+            log("simulated split", key, sim[key]["imbalance_max_over_mean"])
 
     line = {"metric": metric, "value": value, "unit": "edges/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -444,7 +686,8 @@ def main():
             "config": config, "counts": {k: int(v) for k, v in total_counts.items()},
             "kernel_ms_per_step": kms, "wall_s_timed": wall,
             "gpu_launches": launches, "clocks": clocks, "roofline": roof,
-            "cpu_baseline": cpu, "e2e": e2e, "build": build_info}
+            "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "balance": balance,
+            "partition_sim": sim, "kernel_family": family, "build": build_info}
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:

@@ -58,7 +58,7 @@
 extern "C" {
 #endif
 
-#define G2M_ABI_VERSION 3
+#define G2M_ABI_VERSION 4
 
 #define G2M_OK 0
 #define G2M_EUSAGE 1
@@ -99,7 +99,14 @@ typedef struct g2m_task_spec {
     int32_t kind;           /* G2M_TASKS_EDGE / G2M_TASKS_VERTEX */
     int32_t source;         /* G2M_SRC_* */
     int32_t reduced;        /* IMPLICIT/INDEX edge lists: only src > dst */
-    int32_t reserved;
+    int32_t weighted;       /* source-partitioned kernels (g2m_clique_count,
+                               g2m_cycle4_count): 1 = the chunks of the
+                               round-robin are runs of consecutive sources of
+                               equal ESTIMATED work (the pattern-aware
+                               workload estimator, PAPER.md:1256-1262,
+                               1309-1322), rr_chunk = sources per chunk on
+                               average (c = alpha * y); 0 = rr_chunk sources
+                               per chunk */
     const int64_t* data;    /* host array for PAIRS (2*count) / VERTICES / INDEX */
     uint64_t count;         /* entries in data (ignored for IMPLICIT) */
     uint64_t rr_chunk;      /* IMPLICIT only: 0 = whole list, else chunked
@@ -177,6 +184,17 @@ int g2m_graph_info_get(const g2m_graph* g, g2m_graph_info* info);
 int g2m_graph_download(const g2m_graph* g, uint64_t* row_offsets, uint32_t* neighbors,
                        uint32_t* labels_or_null);
 int g2m_graph_destroy(g2m_graph* g);
+/* The (degree, id) rank relabelling of g as a new graph (same orientation):
+ * the id space of g2m_clique_count / g2m_cycle4_count. Relabelling it again
+ * is the identity, so vertex partitions of it mean the same source sets for
+ * the specialised kernels and for g2m_run (full-scale parity). Counts of
+ * every pattern are invariant under the renaming (graph.py:224-238). */
+int g2m_graph_rank_copy(const g2m_graph* g, g2m_graph** out);
+/* Algorithmic work of the specialised kernels on g (bench roofline):
+ * family 0 = bitmap k-clique on an oriented graph, 1 = 4-cycle wedges on a
+ * symmetric graph. out[0] operand bytes, out[1] probed ids / wedges,
+ * out[2] counter updates, out[3] sources with work (see g2m.cu). */
+int g2m_kernel_work(const g2m_graph* g, int32_t family, uint64_t* out);
 /* len(EdgeTaskList.implicit(g, reduced=True)) (graph.py:270-286): slots with
  * dst < src, counted on the device (cached with the reduced task offsets). */
 int g2m_graph_reduced_tasks(const g2m_graph* g, uint64_t* out);

@@ -817,15 +817,16 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
 // (CTA, W = 2,4,8,16), 7: 1024 < d <= max_cta_d (CTA, W = 64; k = 3 only),
 // 6: d > max_cta_d (generic kernel). span_max[c]: widest id window of class c.
 __global__ void k_clique_bucket(const u64* off, const u32* nbr, u64 nv, int kmin1, u64 max_cta_d, u64 pair_maxd,
-                                u64 rr_chunk, u32 parts, u32 part, u32* lists, u64 list_stride, u64* sizes,
-                                u32* span_max) {
+                                u64 rr_chunk, u32 parts, u32 part, const u64* wpre, u64 wchunk, u32* lists,
+                                u64 list_stride, u64* sizes, u32* span_max) {
     for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x) {
-        if (rr_chunk && ((v / rr_chunk) % parts) != part) continue;
+        if (!g2m_owns(v, rr_chunk, parts, part, wpre, wchunk)) continue;
         const u64 b = off[v];
         const u64 d = off[v + 1] - b;
         int c;
         if (d < (u64)kmin1 || d == 0) continue;
-        if (d <= pair_maxd) c = 8;
+        if (max_cta_d == 0) c = 6;   // every source to the generated plan kernel
+        else if (d <= pair_maxd) c = 8;
         else if (d <= 64) c = 1;
         else if (d <= 128) c = 2;
         else if (d <= 256) c = 3;

@@ -27,7 +27,8 @@
 //                     memory -- streaming HBM traffic instead of random
 //                     counter updates
 //   4: larger         all blocks on one v1 at a time, dense counters shared
-//                     by the grid (n words, L2-resident), cleared by memset
+//                     by the grid, one L2-sized id range per pass, cleared
+//                     by memset
 #pragma once
 
 #include "g2m_device.cuh"
@@ -339,16 +340,21 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
 // The v1's wedges are flattened over the grid: k_c4_rows writes each row's
 // wedge count and first nbr index, a scan makes the ends, and k_c4_grid's
 // warps take 1024-element steps (owner row by binary search over the ends),
-// so a few huge rows do not serialise the grid.
-__global__ void k_c4_rows(const u64* __restrict__ off, const u32* __restrict__ nbr, u32 r1, u32 l1, u32 lo_x,
-                          u64* rn_out, u64* rb_out) {
+// so a few huge rows do not serialise the grid. The wedge ends are counted
+// one id range [lo, hi) at a time: dense counters for the range only, sized
+// to stay L2-resident whatever |V| is (RMAT-27: 134 M ids would be 537 MB of
+// counters, random atomics in HBM). Rows are sorted, so N(v) ∩ [lo, hi) is
+// one contiguous segment: the passes partition the wedges, the only extra
+// work per pass is two binary searches per row.
+__global__ void k_c4_rows(const u64* __restrict__ off, const u32* __restrict__ nbr, u32 r1, u32 l1, u32 lo,
+                          u32 hi, u64* rn_out, u64* rb_out) {
     const u32* L = nbr + __ldg(off + r1);
     for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < l1; i += gridDim.x * blockDim.x) {
         const u32 v = __ldg(L + i);
         u64 ro = __ldg(off + v);
         const u32 dv = (u32)(__ldg(off + v + 1) - ro);
-        const u32 s0 = (dv && __ldg(nbr + ro) < lo_x) ? g2m_lb(nbr + ro, dv, lo_x) : 0u;
-        const u32 e1 = (dv && __ldg(nbr + ro + dv - 1) < r1) ? dv : g2m_lb(nbr + ro, dv, r1);
+        const u32 s0 = (dv && __ldg(nbr + ro) < lo) ? g2m_lb(nbr + ro, dv, lo) : 0u;
+        const u32 e1 = (dv && __ldg(nbr + ro + dv - 1) < hi) ? dv : g2m_lb(nbr + ro, dv, hi);
         rn_out[i] = e1 > s0 ? e1 - s0 : 0u;
         rb_out[i] = ro + s0;
     }
@@ -362,7 +368,7 @@ __global__ void k_c4_base(u32 l1, const u64* __restrict__ rn, u64* rb, const u64
 
 __global__ void __launch_bounds__(512)
 k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const u64* __restrict__ rb,
-          const u64* __restrict__ re, u64* ctr, u32* dense, u64* count) {
+          const u64* __restrict__ re, u64* ctr, u32* dense, u32 lo, u64* count) {
     const u32 lane = g2m_lane();
     const u64 tot = re[l1 - 1];
     u64 acc = 0;
@@ -383,7 +389,7 @@ k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const
             const u64 e = e0 + k + lane;
             if (e < tot) {
                 while (__ldg(re + ow) <= e) ++ow;
-                acc += atomicAdd(dense + __ldg(nbr + __ldg(rb + ow) + e), 1u);
+                acc += atomicAdd(dense + (__ldg(nbr + __ldg(rb + ow) + e) - lo), 1u);
             }
         }
     }
@@ -395,11 +401,12 @@ k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const
 // W = Σ_{v ∈ N<(r)} d(v); class 1..4 as above (0: l1 < 2, no cycle).
 // One warp per vertex.
 __global__ void k_c4_bucket(const u64* off, const u32* nbr, u64 nv, u64 rr_chunk, u32 parts, u32 part,
-                            u64 stage_cap, u32* lists, u32* lows, u64* wkeys, u64 stride, u64* sizes) {
+                            const u64* wpre, u64 wchunk, u64 stage_cap, u32* lists, u32* lows, u64* wkeys,
+                            u64 stride, u64* sizes) {
     const u32 lane = g2m_lane();
     for (u64 r = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; r < nv;
          r += ((u64)gridDim.x * blockDim.x) >> 5) {
-        if (rr_chunk && ((r / rr_chunk) % parts) != part) continue;
+        if (!g2m_owns(r, rr_chunk, parts, part, wpre, wchunk)) continue;
         const u64 b = off[r];
         const u32 d = (u32)(off[r + 1] - b);
         const u32 l1 = g2m_wlb(nbr + b, d, (u32)r);

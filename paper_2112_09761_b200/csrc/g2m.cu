@@ -163,6 +163,11 @@ struct DevState {
     DevBuf frontier;         // BFS level-3 frontier items (grow-only)
     DevBuf c4slab;           // 4-cycle staging slabs, one per block
     DevBuf hubs;             // [0] = count, then the hub rows of a row pass (rows longer than kHubRow)
+    // side streams: independent kernel tiers run concurrently so one tier's
+    // tail overlaps the next tier's work (fork/join through events)
+    static constexpr int kSide = 8;
+    cudaStream_t side[kSide] = {};
+    cudaEvent_t evfork = nullptr, evjoin[kSide] = {};
 };
 
 static std::mutex g_dev_mu;
@@ -180,6 +185,11 @@ static int dev_state(int dev, DevState** out) {
         G2M_CUDA(cudaEventCreate(&st->ev1));
         G2M_CUDA(cudaEventCreate(&st->evs0));
         G2M_CUDA(cudaEventCreate(&st->evs1));
+        G2M_CUDA(cudaEventCreateWithFlags(&st->evfork, cudaEventDisableTiming));
+        for (int i = 0; i < DevState::kSide; ++i) {
+            G2M_CUDA(cudaStreamCreateWithFlags(&st->side[i], cudaStreamNonBlocking));
+            G2M_CUDA(cudaEventCreateWithFlags(&st->evjoin[i], cudaEventDisableTiming));
+        }
         G2M_CUDA(cudaDeviceGetAttribute(&st->sms, cudaDevAttrMultiProcessorCount, dev));
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -211,8 +221,16 @@ struct g2m_graph {
     DevBuf rk_off, rk_nbr;
     bool has_rank = false;
     uint64_t rk_deg1 = 0;    // ranks [0, rk_deg1) have degree <= 1
+    // oriented graphs: rank-space rows holding a column <= their row, i.e. DAG
+    // edges against the (degree, id) order (an input oriented some other way)
+    uint64_t rk_down = 0;
     // symmetric graphs: degree orientation, lazily built (diamond support)
     std::unique_ptr<g2m_graph> oriented_copy;
+    // workload estimator: exclusive prefix of per-source estimated work in
+    // rank space (wpre[nv] = total), for the last (kernel family, k) asked
+    DevBuf wpre;
+    int wpre_key = -1;
+    uint64_t wpre_total = 0, wpre_sources = 0;
 };
 
 // out[0] = max degree, out[1] = Σ degree² (the BFS frontier bound, executor.choose_search)
@@ -985,6 +1003,18 @@ k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_
     }
 }
 
+// Rows are ascending, so a row points against the order iff its first column
+// is not above the row.
+__global__ void k_rank_down_rows(const u64* off, const u32* nbr, u64 nv, u64* out) {
+    u64 c = 0;
+    for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < nv; r += (u64)gridDim.x * blockDim.x) {
+        const u64 b = off[r];
+        if (off[r + 1] > b && (u64)__ldg(nbr + b) <= r) ++c;
+    }
+    c = g2m_wsum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 __global__ void k_low_bits(const u64* keys, u64 n, int rb, u32* out) {
     const u64 mask = ((u64)1 << rb) - 1;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
@@ -1077,6 +1107,16 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
         k_low_bits<<<grid_for(st, slots, 256), 256, 0, st->stream>>>(s64, slots, rb, g->rk_nbr.as<u32>());
         G2M_CUDA(cudaGetLastError());
     }
+    if (nv && slots && g->oriented) {
+        G2M_TRY(st->tmp2.ensure(8));
+        u64* dn = st->tmp2.as<u64>();
+        G2M_CUDA(cudaMemsetAsync(dn, 0, 8, st->stream));
+        ++st->launches;
+        k_rank_down_rows<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), nv,
+                                                                          dn);
+        G2M_CUDA(cudaGetLastError());
+        G2M_CUDA(cudaMemcpyAsync(&g->rk_down, dn, 8, cudaMemcpyDeviceToHost, st->stream));
+    }
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     phase("rows");
     g->has_rank = true;
@@ -1091,6 +1131,142 @@ extern "C" int g2m_graph_reduced_tasks(const g2m_graph* g, uint64_t* out) {
     G2M_CUDA(cudaSetDevice(g->dev));
     G2M_TRY(ensure_reduced(g, st));
     *out = g->red_total;
+    return G2M_OK;
+}
+
+// ---- the specialised kernels' own algorithmic work (bench roofline) ---------
+// out[0] = operand bytes the algorithm must read at least once (the CSR words
+// and offsets it consumes; served by L2 or HBM), out[1] = the unit count the
+// cost is linear in, out[2] = updates of counters (4 B read-modify-write
+// each), out[3] = sources with work.
+//   family 0, k-clique on an oriented graph (bitmap local graphs): per source u
+//     the offsets and N+(u), then for each v in N+(u) its offsets and N+(v)
+//     (the local-graph probes): 16 n + 20 m + 4 Σ_v d-(v) d+(v);
+//     out[1] = Σ_v d-(v) d+(v) (probed ids).
+//   family 1, 4-cycle on a symmetric graph (wedge aggregation, rank space):
+//     per top vertex r its offsets and N<(r), per v in N<(r) its offsets and
+//     the wedge ends N(v) ∩ [lo_x, r): 16 n + 20 Σ_r l(r) + 4 W; out[1] = W
+//     wedges, out[2] = W counter increments.
+__global__ void k_work_clique(const u64* off, const u32* nbr, u64 nv, const u32* indeg, u64* out) {
+    u64 probes = 0, src = 0;
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x) {
+        const u64 d = off[v + 1] - off[v];
+        probes += d * (u64)indeg[v];
+        src += d ? 1 : 0;
+    }
+    probes = g2m_wsum(probes);
+    src = g2m_wsum(src);
+    if ((threadIdx.x & 31) == 0) {
+        if (probes) atomicAdd(out, probes);
+        if (src) atomicAdd(out + 1, src);
+    }
+}
+
+__global__ void k_work_c4(const u64* off, const u32* nbr, u64 nv, u32 lo_x, u64* out) {
+    const u32 lane = g2m_lane();
+    u64 w = 0, lsum = 0, src = 0;
+    for (u64 r = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; r < nv;
+         r += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u64 b = off[r];
+        const u32 d = (u32)(off[r + 1] - b);
+        const u32 l1 = g2m_wlb(nbr + b, d, (u32)r);
+        if (l1 < 2) continue;
+        for (u32 i = lane; i < l1; i += 32) {
+            const u32 v = __ldg(nbr + b + i);
+            const u64 ro = __ldg(off + v);
+            const u32 dv = (u32)(__ldg(off + v + 1) - ro);
+            const u32 s0 = g2m_lb(nbr + ro, dv, lo_x), e1 = g2m_lb(nbr + ro, dv, (u32)r);
+            w += e1 > s0 ? e1 - s0 : 0;
+        }
+        if (lane == 0) {
+            lsum += l1;
+            ++src;
+        }
+    }
+    w = g2m_wsum(w);
+    if (lane == 0) {
+        if (w) atomicAdd(out, w);
+        if (lsum) atomicAdd(out + 1, lsum);
+        if (src) atomicAdd(out + 2, src);
+    }
+}
+
+extern "C" int g2m_kernel_work(const g2m_graph* g, int32_t family, uint64_t* out) {
+    if (!g || !out) return fail(G2M_EUSAGE, "null argument");
+    if (family == 0 && !g->oriented) return fail(G2M_EUSAGE, "clique work needs an oriented graph");
+    if (family == 1 && g->oriented) return fail(G2M_EUSAGE, "4-cycle work needs a symmetric graph");
+    if (family != 0 && family != 1) return fail(G2M_EUSAGE, "unknown kernel family");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    const u64 nv = g->nv;
+    DevBuf acc, indeg;
+    G2M_TRY(acc.ensure(4 * 8));
+    G2M_CUDA(cudaMemsetAsync(acc.p, 0, 4 * 8, st->stream));
+    uint64_t h[4] = {0, 0, 0, 0};
+    if (family == 0) {
+        G2M_TRY(indeg.ensure(std::max<u64>(nv, 1) * 4));
+        G2M_CUDA(cudaMemsetAsync(indeg.p, 0, std::max<u64>(nv, 1) * 4, st->stream));
+        if (g->slots) {
+            ++st->launches;
+            k_rank_indeg<<<grid_for(st, g->slots, 256), 256, 0, st->stream>>>(g->nbr.as<u32>(), g->slots,
+                                                                                indeg.as<u32>());
+        }
+        if (nv) {
+            ++st->launches;
+            k_work_clique<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), nv,
+                                                                            indeg.as<u32>(), acc.as<u64>());
+        }
+        G2M_CUDA(cudaGetLastError());
+        G2M_CUDA(cudaMemcpyAsync(h, acc.p, 16, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        out[1] = h[0];
+        out[0] = 16 * nv + 20 * g->slots + 4 * h[0];
+        out[2] = 0;
+        out[3] = h[1];
+        return G2M_OK;
+    }
+    G2M_TRY(ensure_rank(g, st));
+    if (nv) {
+        ++st->launches;
+        k_work_c4<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), nv,
+                                                                        (u32)g->rk_deg1, acc.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_CUDA(cudaMemcpyAsync(h, acc.p, 24, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    out[1] = h[0];
+    out[0] = 16 * nv + 20 * h[1] + 4 * h[0];
+    out[2] = h[0];
+    out[3] = h[2];
+    return G2M_OK;
+}
+
+// The (degree, id) rank relabelling as a graph of its own (same orientation
+// flag): the id space the bitmap-LGS and wedge kernels work in. Relabelling
+// it again is the identity, so a chunked round-robin share of its vertices is
+// the same source set for those kernels and for the generated plan kernel
+// (bench parity at full scale).
+extern "C" int g2m_graph_rank_copy(const g2m_graph* g, g2m_graph** out) {
+    if (!g || !out) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    G2M_TRY(ensure_rank(g, st));
+    auto r = std::make_unique<g2m_graph>();
+    r->dev = g->dev;
+    r->nv = g->nv;
+    r->slots = g->slots;
+    r->oriented = g->oriented;
+    G2M_TRY(r->off.ensure((g->nv + 1) * 8));
+    G2M_TRY(r->nbr.ensure(std::max<u64>(g->slots, 1) * 4));
+    G2M_CUDA(cudaMemcpyAsync(r->off.p, g->rk_off.p, (g->nv + 1) * 8, cudaMemcpyDeviceToDevice, st->stream));
+    if (g->slots)
+        G2M_CUDA(cudaMemcpyAsync(r->nbr.p, g->rk_nbr.p, g->slots * 4, cudaMemcpyDeviceToDevice, st->stream));
+    G2M_TRY(finish_graph(r.get(), st));
+    *out = r.release();
     return G2M_OK;
 }
 
@@ -1667,45 +1843,51 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     u64* next = ctr + 2;     // one work counter per launch
     int slot = 0;
     const bool dbg = getenv("G2M_DEBUG") != nullptr;
+    // The tiers are independent (own work counter, atomic 128-bit count), so
+    // they run on the side streams concurrently: a persistent tier's blocks
+    // retire as its queue drains and the next tier's blocks take the SMs, so
+    // tails overlap instead of draining the GPU between launches. The mining
+    // time is the fork -> join span on the main stream. G2M_DEBUG or
+    // G2M_SERIAL_TIERS serialise them with one timed launch each.
+    const bool serial = dbg || getenv("G2M_SERIAL_TIERS") != nullptr;
+    int nside = 0;
+    G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
     auto timed = [&](auto&& fn) -> int {
-        G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
-        fn();
+        if (!serial) {
+            // ordered after everything on the main stream so far (incl. allocations)
+            cudaStream_t s = st->side[nside % DevState::kSide];
+            G2M_CUDA(cudaEventRecord(st->evfork, st->stream));
+            G2M_CUDA(cudaStreamWaitEvent(s, st->evfork, 0));
+            fn(s);
+            G2M_CUDA(cudaGetLastError());
+            ++nside;
+            return G2M_OK;
+        }
+        cudaEvent_t a = nullptr;
+        G2M_CUDA(cudaEventCreate(&a));
+        G2M_CUDA(cudaEventRecord(a, st->stream));
+        fn(st->stream);
         G2M_CUDA(cudaGetLastError());
         G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
         G2M_CUDA(cudaEventSynchronize(st->ev1));
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, st->ev0, st->ev1);
-        *kms += ms;
+        cudaEventElapsedTime(&ms, a, st->ev1);
+        cudaEventDestroy(a);
         if (dbg) fprintf(stderr, "[g2m]   launch %d: %.3f ms\n", slot, ms);
         return G2M_OK;
     };
-    if (kClasses > 8 && sizes[8]) {
-        constexpr int WPB = 8;
-        u64 grab = std::max<u64>(1, std::min<u64>(16, sizes[8] / ((u64)st->sms * 64 * WPB)));
-        G2M_TRY(timed([&] {
-            ++st->launches;
-            if constexpr (K == 3)
-                k_clique_pairs<K, WPB, 256><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
-                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
-            else if constexpr (K == 4)
-                k_clique_pairs<K, WPB, 128><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
-                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
-            else
-                k_clique_pairs<K, WPB><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
-                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
-        }));
-        ++slot;
-    }
-    if (sizes[1]) {
-        constexpr int WPB = 8;
-        u64 grab = std::max<u64>(1, std::min<u64>(8, sizes[1] / ((u64)st->sms * 64 * WPB)));
-        G2M_TRY(timed([&] {
-            ++st->launches;
-            k_clique_warp<K, WPB, SUP><<<st->sms * 8, WPB * 32, 0, st->stream>>>(
-                off, nbr, lists + 1 * stride, sizes[1], next + slot, grab, count, tsup);
-        }));
-        ++slot;
-    }
+    auto join = [&]() -> int {
+        for (int i = 0; i < std::min(nside, DevState::kSide); ++i) {
+            G2M_CUDA(cudaEventRecord(st->evjoin[i], st->side[i]));
+            G2M_CUDA(cudaStreamWaitEvent(st->stream, st->evjoin[i], 0));
+        }
+        G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
+        G2M_CUDA(cudaEventSynchronize(st->ev1));
+        float ms = 0.f;
+        G2M_CUDA(cudaEventElapsedTime(&ms, st->ev0, st->ev1));
+        *kms += ms;
+        return G2M_OK;
+    };
     int max_smem = 0;
     G2M_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
     int sm_smem = 0;
@@ -1745,9 +1927,9 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         if (dbg)
             fprintf(stderr, "[g2m] clique k=%d class %d: %llu sources, W=%d NW=%d%s, window<=%u bits, bitmap %u bits, smem %zu, %d CTA/SM\n",
                     K, cls, (unsigned long long)sizes[cls], W, NW, GR ? " (rows in L2)" : "", spans[cls], bmw * 32, smem, occ);
-        G2M_TRY(timed([&] {
+        G2M_TRY(timed([&](cudaStream_t ss) {
             ++st->launches;
-            kern<<<(unsigned)grid, NW * 32, smem, st->stream>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
+            kern<<<(unsigned)grid, NW * 32, smem, ss>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
                                                                  next + slot, count, bmw, grows, tsup, split,
                                                                  direct_max);
         }));
@@ -1756,9 +1938,13 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     };
     using std::integral_constant;
     using F = std::false_type;
-    G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 16>{}, F{}, 2, 2));
-    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, F{}, 3, 3));
-    G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, F{}, 4, 2));
+    // heaviest sources first (longest-processing-time order): the tiers with
+    // few, large local graphs start at once and the fine-grained tiers fill
+    // the SMs their tails leave idle
+    if constexpr (K == 3)
+        G2M_TRY(cta(integral_constant<int, 64>{}, integral_constant<int, 32>{}, F{}, 7, 1));
+    else
+        G2M_TRY(cta(integral_constant<int, 32>{}, integral_constant<int, 16>{}, std::true_type{}, 7, 1));
     // one block per SM (the 139 KB of rows allow no second): as many warps as the
     // per-warp candidate lists leave room for
     if constexpr (K == 4)
@@ -1767,10 +1953,109 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 24>{}, F{}, 5, 1));
     else   // k = 3: no rows; two blocks per SM, windows beyond the bitmap go two-level
         G2M_TRY(cta(integral_constant<int, 16>{}, integral_constant<int, 16>{}, F{}, 5, 2));
-    if constexpr (K == 3)
-        G2M_TRY(cta(integral_constant<int, 64>{}, integral_constant<int, 32>{}, F{}, 7, 1));
-    else
-        G2M_TRY(cta(integral_constant<int, 32>{}, integral_constant<int, 16>{}, std::true_type{}, 7, 1));
+    G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, F{}, 4, 2));
+    G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, F{}, 3, 3));
+    G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 16>{}, F{}, 2, 2));
+    if (kClasses > 8 && sizes[8]) {
+        constexpr int WPB = 8;
+        u64 grab = std::max<u64>(1, std::min<u64>(16, sizes[8] / ((u64)st->sms * 64 * WPB)));
+        G2M_TRY(timed([&](cudaStream_t ss) {
+            ++st->launches;
+            if constexpr (K == 3)
+                k_clique_pairs<K, WPB, 256><<<st->sms * 8, WPB * 32, 0, ss>>>(
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
+            else if constexpr (K == 4)
+                k_clique_pairs<K, WPB, 128><<<st->sms * 8, WPB * 32, 0, ss>>>(
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
+            else
+                k_clique_pairs<K, WPB><<<st->sms * 8, WPB * 32, 0, ss>>>(
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
+        }));
+        ++slot;
+    }
+    if (sizes[1]) {
+        constexpr int WPB = 8;
+        u64 grab = std::max<u64>(1, std::min<u64>(8, sizes[1] / ((u64)st->sms * 64 * WPB)));
+        G2M_TRY(timed([&](cudaStream_t ss) {
+            ++st->launches;
+            k_clique_warp<K, WPB, SUP><<<st->sms * 8, WPB * 32, 0, ss>>>(
+                off, nbr, lists + 1 * stride, sizes[1], next + slot, grab, count, tsup);
+        }));
+        ++slot;
+    }
+    return join();   // before `slab` (used on a side stream) is released on the main stream
+}
+
+// ---- pattern-aware workload estimator ----
+// Per source vertex of the rank-space graph, the estimated work of its
+// search, one warp per source:
+//   k-clique (bitmap LGS): Σ_{v ∈ N+(u)} d+(v) (the local-graph probes) +
+//                          d+(u) * ceil(d+(u)/32) * (k - 2) (row words per level)
+//   4-cycle (wedges):      Σ_{v ∈ N(r), v < r} d(v) (the wedge bound of r)
+// The partition deals runs of consecutive sources of equal estimated work
+// round-robin (g2m_owns), so a chunk of hub sources is as heavy as a chunk
+// of thousands of leaves.
+__global__ void k_source_cost(const u64* off, const u32* nbr, u64 nv, int kind, int k, u64* cost, u64* nz) {
+    const u32 lane = g2m_lane();
+    u64 cnt = 0;
+    for (u64 r = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; r < nv;
+         r += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u64 b = off[r];
+        const u32 d = (u32)(off[r + 1] - b);
+        const u32 l = kind == 0 ? d : g2m_wlb(nbr + b, d, (u32)r);
+        u64 w = 0;
+        if (l >= (kind == 0 ? (u32)(k - 1) : 2u)) {
+            for (u32 i = lane; i < l; i += 32) {
+                const u32 v = __ldg(nbr + b + i);
+                w += __ldg(off + v + 1) - __ldg(off + v);
+            }
+            w = g2m_wsum(w);
+            if (kind == 0) w += (u64)d * ((d + 31) / 32) * (u64)(k - 2);
+        }
+        if (lane == 0) {
+            cost[r] = w;
+            cnt += w ? 1 : 0;
+        }
+    }
+    if (lane == 0 && cnt) atomicAdd(nz, cnt);
+}
+
+// wpre/wchunk for a weighted partition `part` of the rank-space graph g
+// (kind 0 clique of size k, 1 4-cycle); nullptr/0 when not weighted.
+static int source_weights(const g2m_graph* cg, DevState* st, const g2m_task_spec* part, int kind, int k,
+                          const u64** wpre, u64* wchunk) {
+    *wpre = nullptr;
+    *wchunk = 0;
+    if (!part || !part->weighted || !part->rr_chunk) return G2M_OK;
+    g2m_graph* g = const_cast<g2m_graph*>(cg);
+    const u64 nv = g->nv;
+    const int key = kind * 16 + k;
+    if (g->wpre_key != key) {
+        G2M_TRY(g->wpre.ensure((nv + 1) * 8));
+        G2M_TRY(st->tmp2.ensure((nv + 1) * 8 + 8));
+        u64* cost = st->tmp2.as<u64>();
+        u64* nz = cost + nv + 1;
+        G2M_CUDA(cudaMemsetAsync(cost, 0, (nv + 1) * 8 + 8, st->stream));
+        if (nv) {
+            ++st->launches;
+            k_source_cost<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(g->rk_off.as<u64>(), g->rk_nbr.as<u32>(),
+                                                                                 nv, kind, k, cost, nz);
+            G2M_CUDA(cudaGetLastError());
+        }
+        G2M_TRY(exclusive_scan_u64(st, cost, g->wpre.as<u64>(), nv));
+        uint64_t h[2] = {0, 0};
+        G2M_CUDA(cudaMemcpyAsync(h, g->wpre.as<u64>() + nv, 8, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaMemcpyAsync(h + 1, nz, 8, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        g->wpre_total = h[0];
+        g->wpre_sources = h[1];
+        g->wpre_key = key;
+    }
+    // as many chunks as chunks of rr_chunk sources there are (c = alpha * y),
+    // each carrying an equal share of the estimated work
+    const u64 nchunks = std::max<u64>(1, g->wpre_sources / part->rr_chunk);
+    *wchunk = std::max<u64>(1, (g->wpre_total + nchunks - 1) / nchunks);
+    *wpre = g->wpre.as<u64>();
     return G2M_OK;
 }
 
@@ -1810,6 +2095,9 @@ static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
     G2M_TRY(ensure_rank(g, st));
     const u64* off = g->rk_off.as<u64>();
     const u32* nbr = g->rk_nbr.as<u32>();
+    const u64* wpre = nullptr;
+    u64 wchunk = 0;
+    G2M_TRY(source_weights(g, st, part, 0, k, &wpre, &wchunk));
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
     // counters: ctr[8..9] count (lo, hi), ctr[10..] one work counter per launch
     G2M_TRY(st->counters.ensure(32 * 8));
@@ -1823,10 +2111,13 @@ static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
     G2M_CUDA(cudaMemsetAsync(dsizes, 0, kClasses * 12, st->stream));
     if (g->nv) {
         ++st->launches;
+        // a DAG not oriented by (degree, id) (Graph(..., oriented=True) from another
+        // orientation) breaks the tiers' "edges point up" invariant: every source
+        // then takes the generated plan kernel (max_cta_d = 0)
         g2m_clique::k_clique_bucket<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(
-            off, nbr, g->nv, k - 1, k == 3 ? 4096 : 2048,
-            k == 3 ? pair_maxd_tc(g->nv) : (k == 4 ? pair_maxd3() : pair_maxd()), rr_chunk, parts, pt,
-            st->tasks_b.as<u32>(),
+            off, nbr, g->nv, k - 1, g->rk_down ? 0 : (k == 3 ? 4096 : 2048),
+            k == 3 ? pair_maxd_tc(g->nv) : (k == 4 ? pair_maxd3() : pair_maxd()), rr_chunk, parts, pt, wpre,
+            wchunk, st->tasks_b.as<u32>(),
             stride, dsizes, dspans);
         G2M_CUDA(cudaGetLastError());
     }
@@ -1957,7 +2248,7 @@ extern "C" int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, 
     if (og->nv) {
         ++st->launches;
         g2m_clique::k_clique_bucket<<<grid_for(st, og->nv, 256), 256, 0, st->stream>>>(
-            off, nbr, og->nv, 2, 4096, 0, 0, 1, 0, st->tasks_b.as<u32>(), stride, dsizes, dspans);
+            off, nbr, og->nv, 2, 4096, 0, 0, 1, 0, nullptr, 0, st->tasks_b.as<u32>(), stride, dsizes, dspans);
         G2M_CUDA(cudaGetLastError());
     }
     uint64_t sizes[kClasses];
@@ -2036,6 +2327,9 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
     const u32* nbr = g->rk_nbr.as<u32>();
     const u64 nv = g->nv;
     const u32 lo_x = (u32)g->rk_deg1;
+    const u64* wpre = nullptr;
+    u64 wchunk = 0;
+    G2M_TRY(source_weights(g, st, part, 1, 4, &wpre, &wchunk));
     const bool dbg = getenv("G2M_DEBUG") != nullptr;
     constexpr int NW = 16;
     // tier 3 setup: bucket array in shared memory, staging slab per block
@@ -2075,7 +2369,7 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
     if (nv) {
         ++st->launches;
         g2m_c4::k_c4_bucket<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(
-            off, nbr, nv, rr_chunk, parts, pt, stage_cap, lists, lows, wkeys, stride, dsizes);
+            off, nbr, nv, rr_chunk, parts, pt, wpre, wchunk, stage_cap, lists, lows, wkeys, stride, dsizes);
         G2M_CUDA(cudaGetLastError());
     }
     uint64_t sizes[5];
@@ -2102,7 +2396,11 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
     int slot = 0;
     auto timed = [&](auto&& fn) -> int {
         G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
-        fn();
+        if constexpr (std::is_same_v<decltype(fn()), int>) {
+            G2M_TRY(fn());
+        } else {
+            fn();
+        }
         G2M_CUDA(cudaGetLastError());
         G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
         G2M_CUDA(cudaEventSynchronize(st->ev1));
@@ -2173,14 +2471,18 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
     }
     if (sizes[4]) {
         // one v1 at a time on the whole grid, its wedges flattened over all
-        // warps; counters shared by the grid (n words, L2-resident)
+        // warps; counters shared by the grid for one id range per pass
+        // (G2M_C4_RANGE ids, default 2^24 = 64 MB of counters: L2-resident)
         std::vector<u32> gv(sizes[4]), gl(sizes[4]);
         G2M_CUDA(cudaMemcpyAsync(gv.data(), lists + 4 * stride, sizes[4] * 4, cudaMemcpyDeviceToHost, st->stream));
         G2M_CUDA(cudaMemcpyAsync(gl.data(), lows + 4 * stride, sizes[4] * 4, cudaMemcpyDeviceToHost, st->stream));
         G2M_CUDA(cudaStreamSynchronize(st->stream));
         u32 lmax = 0;
         for (u32 l : gl) lmax = std::max(lmax, l);
-        G2M_TRY(st->tmp1.ensure(stride * 4 + 64));
+        u64 range = (u64)1 << 24;
+        if (const char* e = getenv("G2M_C4_RANGE")) range = std::max<u64>(1024, strtoull(e, nullptr, 10));
+        range = std::min<u64>(range, stride);
+        G2M_TRY(st->tmp1.ensure(range * 4 + 64));
         G2M_TRY(st->tmp2.ensure((u64)lmax * 24 + 64));
         u32* dense = st->tmp1.as<u32>();
         u64* rn = st->tmp2.as<u64>();
@@ -2190,22 +2492,33 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
         size_t tb = 0;
         G2M_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, rn, re, (int64_t)lmax, st->stream));
         G2M_TRY(st->cub_tmp.ensure(tb));
-        G2M_CUDA(cudaMemsetAsync(dense, 0, stride * 4, st->stream));
-        G2M_TRY(timed([&] {
+        G2M_CUDA(cudaMemsetAsync(dense, 0, range * 4, st->stream));
+        u64 passes = 0;
+        G2M_TRY(timed([&]() -> int {
             for (u64 q = 0; q < sizes[4]; ++q) {
                 const u32 r1 = gv[q], l1 = gl[q];
-                ++st->launches;
-                g2m_c4::k_c4_rows<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(off, nbr, r1, l1, lo_x, rn, rb);
-                size_t t2 = tb;
-                cub::DeviceScan::InclusiveSum(st->cub_tmp.p, t2, rn, re, (int64_t)l1, st->stream);
-                ++st->launches;
-                g2m_c4::k_c4_base<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(l1, rn, rb, re);
-                cudaMemsetAsync(gctr, 0, 8, st->stream);
-                ++st->launches;
-                g2m_c4::k_c4_grid<<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rn, rb, re, gctr, dense, count);
-                cudaMemsetAsync(dense, 0, (size_t)r1 * 4, st->stream);
+                for (u64 lo = lo_x; lo < r1; lo += range) {
+                    const u32 hi = (u32)std::min<u64>(r1, lo + range);
+                    ++passes;
+                    ++st->launches;
+                    g2m_c4::k_c4_rows<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(off, nbr, r1, l1, (u32)lo, hi,
+                                                                                       rn, rb);
+                    size_t t2 = tb;
+                    G2M_CUDA(cub::DeviceScan::InclusiveSum(st->cub_tmp.p, t2, rn, re, (int64_t)l1, st->stream));
+                    ++st->launches;
+                    g2m_c4::k_c4_base<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(l1, rn, rb, re);
+                    G2M_CUDA(cudaMemsetAsync(gctr, 0, 8, st->stream));
+                    ++st->launches;
+                    g2m_c4::k_c4_grid<<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rn, rb, re, gctr, dense,
+                                                                           (u32)lo, count);
+                    G2M_CUDA(cudaGetLastError());
+                    G2M_CUDA(cudaMemsetAsync(dense, 0, (size_t)(hi - lo) * 4, st->stream));
+                }
             }
+            return G2M_OK;
         }));
+        if (dbg) fprintf(stderr, "[g2m] cycle4 grid tier: %llu sources, %llu range passes of <= %llu ids\n",
+                         (unsigned long long)sizes[4], (unsigned long long)passes, (unsigned long long)range);
     }
     uint64_t h[2] = {0, 0};
     G2M_CUDA(cudaMemcpyAsync(h, count, 16, cudaMemcpyDeviceToHost, st->stream));

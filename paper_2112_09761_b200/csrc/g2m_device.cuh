@@ -22,6 +22,15 @@ typedef long long i64;
 
 #define G2M_FULL 0xffffffffu
 
+// Does this partition own source r? Chunked round-robin over sources:
+// chunk = r / rr_chunk, or with the workload estimator (wpre = exclusive
+// prefix of per-source estimated work) chunk = wpre[r] / wchunk, i.e.
+// consecutive sources of equal estimated work.
+__device__ __forceinline__ bool g2m_owns(u64 r, u64 rr_chunk, u32 parts, u32 part, const u64* wpre, u64 wchunk) {
+    if (wpre) return ((wpre[r] / wchunk) % parts) == part;
+    return !rr_chunk || ((r / rr_chunk) % parts) == part;
+}
+
 // Bounded-frontier BFS work item: level-3 candidates [lo, lo + fchunk) of
 // level-3 node `node` under the edge task (v1, v2).
 struct G2MItem {

@@ -18,12 +18,30 @@ LIMBS = 4
 _MASK = (1 << 32) - 1
 
 
-def shard(rank: int, world: int, chunk: int = 256):
+ALPHA = 2     # c = ALPHA * y
+
+
+def resident_warps(device: int = 0) -> int:
+    """y of the paper's chunk rule: warps resident on one GPU at once."""
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(device)
+        return int(p.multi_processor_count * p.max_threads_per_multi_processor // 32)
+    except Exception:
+        return 148 * 64     # B200: 148 SMs x 64 warps
+
+
+def shard(rank: int, world: int, chunk: int | None = None, device: int = 0):
     """The (rr_chunk, rr_parts, rr_part) triple of this rank's chunked
-    round-robin share (scheduler.split_chunked_rr's queue ``rank``)."""
+    round-robin share (scheduler.split_chunked_rr's queue ``rank``) with the
+    paper's chunk c = ALPHA * y edge tasks, y = resident warps. The
+    source-partitioned kernels split sources instead, by the workload
+    estimator (executor.source_spec)."""
     if world < 1 or not (0 <= rank < world):
         raise ValueError(f"bad rank {rank} of {world}")
-    return None if world == 1 else (chunk, world, rank)
+    if world == 1:
+        return None
+    return (int(chunk) if chunk else ALPHA * resident_warps(device), world, rank)
 
 
 def to_limbs(v: int) -> list[int]:

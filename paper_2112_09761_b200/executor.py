@@ -324,6 +324,42 @@ def _is_diamond_count(g: Graph, forest: PlanForest, tasks, sink, index, rr) -> b
     return isinstance(tasks, VertexTasks)
 
 
+# How the source-partitioned kernels (bitmap k-clique, 4-cycle wedges) split
+# their sources over the parts of a multi-GPU run: "est" = the pattern-aware
+# workload estimator (runs of consecutive rank-space sources of equal
+# estimated work, SOURCE_CHUNK sources per run on average, dealt round-robin;
+# PAPER.md:1256-1262, 1309-1322), "rr" = sources dealt one by one in rank
+# order. G2M_SOURCE_SPLIT=est[:c] | rr overrides.
+SOURCE_SPLIT = "est"
+SOURCE_CHUNK = 256
+_ss = os.environ.get("G2M_SOURCE_SPLIT")
+if _ss:
+    SOURCE_SPLIT, _, _c = _ss.partition(":")
+    if _c:
+        SOURCE_CHUNK = int(_c)
+
+
+def source_spec(rr, split: str | None = None, chunk: int | None = None) -> N.TaskSpec:
+    """The vertex-partition spec of a source-partitioned kernel for the
+    part rr = (c, n, i) of a chunked round-robin schedule (None: all
+    sources). The edge-task chunk c does not apply: the parts split the
+    *sources* (whose weights differ by orders of magnitude), either by the
+    workload estimator or one by one."""
+    spec = N.TaskSpec()
+    spec.kind = N.TASKS_VERTEX
+    if rr is None:
+        return spec
+    split = split or SOURCE_SPLIT
+    if split == "est":
+        spec.rr_chunk, spec.weighted = int(chunk or SOURCE_CHUNK), 1
+    elif split == "rr":
+        spec.rr_chunk = int(chunk or 1)
+    else:
+        raise ValueError(f"unknown source split {split!r}")
+    spec.rr_parts, spec.rr_part = int(rr[1]), int(rr[2])
+    return spec
+
+
 def kernel_family(g: Graph, forest: PlanForest, tasks, sink=None, index=None, rr=None,
                   lgs: bool = True, instrument: bool = False) -> str:
     """Which kernels ``execute`` runs for this forest: "lgs" (bitmap k-clique),
@@ -407,8 +443,10 @@ def _has_emitters(forest: PlanForest) -> bool:
 def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None = None,
             rr=None, index=None, flatten: bool = True, run_config: N.RunConfig | None = None,
             instrument: bool = False, lgs: bool = True, search: str = "dfs",
-            cfg: ExecutionConfig | None = None):
-    """Run one forest on one GPU. Returns (counts, RunStats, stopped, compile)."""
+            cfg: ExecutionConfig | None = None, source_split: tuple | None = None):
+    """Run one forest on one GPU. Returns (counts, RunStats, stopped, compile).
+    ``source_split`` = (split, chunk) overrides how the source-partitioned
+    kernels split a round-robin part ``rr`` (source_spec)."""
     dev = N.default_device() if device is None else device
     N.require_device(dev)
     dg = g.device_graph(dev)
@@ -418,10 +456,7 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
         # bitmap local-graph kernels; the generated plan kernel handles the
         # few sources whose out-degree exceeds the bitmap tiers
         cp = compile_forest(forest, False, False, dg.max_degree, flatten=flatten)
-        spec = N.TaskSpec()
-        spec.kind = N.TASKS_VERTEX
-        if rr is not None:   # sources of very different weight: deal them one by one
-            spec.rr_chunk, spec.rr_parts, spec.rr_part = 1, rr[1], rr[2]
+        spec = source_spec(rr, *(source_split or ()))
         words = np.zeros(2, dtype=np.uint64)
         stats = N.RunStats()
         cfg = run_config if run_config is not None else N.RunConfig()
@@ -430,10 +465,7 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
         pid = forest.pattern_ids[0]
         return {pid: int(words[0]) | (int(words[1]) << 64)}, stats, False, cp
     if lgs and not instrument and _is_cycle4_count(g, forest, tasks, sink, index):
-        spec = N.TaskSpec()
-        spec.kind = N.TASKS_VERTEX
-        if rr is not None:   # top vertices of very different weight: deal them one by one
-            spec.rr_chunk, spec.rr_parts, spec.rr_part = 1, rr[1], rr[2]
+        spec = source_spec(rr, *(source_split or ()))
         words = np.zeros(2, dtype=np.uint64)
         stats = N.RunStats()
         cfg = run_config if run_config is not None else N.RunConfig()

@@ -89,10 +89,35 @@ def test_gloo_world2_shards_and_reduction():
 
 def test_shard_and_limbs():
     assert D.shard(0, 1) is None
-    assert D.shard(3, 8) == (256, 8, 3)
+    assert D.shard(3, 8, chunk=256) == (256, 8, 3)
+    # c = alpha * y: alpha = 2, y = resident warps
+    assert D.shard(3, 8) == (D.ALPHA * D.resident_warps(), 8, 3)
+    assert D.resident_warps() > 0
     with pytest.raises(ValueError):
         D.shard(8, 8)
     for v in (0, 1, (1 << 32) - 1, 1 << 64, (1 << 128) - 1):
         assert D.from_limbs(D.to_limbs(v)) == v
     with pytest.raises(ValueError):
         D.to_limbs(1 << 128)
+
+
+def test_source_spec_fields():
+    from paper_2112_09761_b200 import executor as EX
+    s = EX.source_spec(None)
+    assert s.rr_chunk == 0 and s.weighted == 0
+    s = EX.source_spec((18944, 8, 3))
+    assert (s.rr_chunk, s.weighted, s.rr_parts, s.rr_part) == (EX.SOURCE_CHUNK, 1, 8, 3)
+    s = EX.source_spec((18944, 8, 3), "rr", 1)
+    assert (s.rr_chunk, s.weighted, s.rr_parts, s.rr_part) == (1, 0, 8, 3)
+    with pytest.raises(ValueError):
+        EX.source_spec((1, 2, 0), "bogus")
+
+
+def test_bench_gpus_mismatch_exits_nonzero():
+    import subprocess
+    import sys
+    from pathlib import Path
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(Path(__file__).resolve().parent.parent / "bench.py"),
+                          "--gpus", "2"], capture_output=True, text=True, env=env, timeout=120)
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stdout
