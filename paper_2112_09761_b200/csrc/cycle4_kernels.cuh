@@ -378,12 +378,11 @@ k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const
         e0 = __shfl_sync(G2M_FULL, e0, 0);
         if (e0 >= tot) break;
         // owner of e0: first row with end > e0
-        u32 lo = 0, n = l1;
+        u32 ow = 0, n = l1;
         while (n > 0) {
             const u32 h = n >> 1;
-            if (__ldg(re + lo + h) <= e0) { lo += h + 1; n -= h + 1; } else n = h;
+            if (__ldg(re + ow + h) <= e0) { ow += h + 1; n -= h + 1; } else n = h;
         }
-        u32 ow = lo;
 #pragma unroll 4
         for (u32 k = 0; k < 1024; k += 32) {
             const u64 e = e0 + k + lane;

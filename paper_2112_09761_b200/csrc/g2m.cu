@@ -1849,13 +1849,28 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     // tails overlap instead of draining the GPU between launches. The mining
     // time is the fork -> join span on the main stream. G2M_DEBUG or
     // G2M_SERIAL_TIERS serialise them with one timed launch each.
+    // Measured (RMAT-22, r02b): concurrent tiers cost k = 3/4 5-12 % (each
+    // tier already fills the GPU; co-resident blocks of two tiers halve the
+    // occupancy each was sized for) and gain k = 5 3 % (its W=16 tier runs
+    // 1 CTA/SM for 589 ms and the small tiers fill the gaps). Default: one
+    // stream without host syncs for k <= 4 (each tier starts as the previous
+    // drains), two side streams for k = 5. G2M_TIER_STREAMS=n overrides.
     const bool serial = dbg || getenv("G2M_SERIAL_TIERS") != nullptr;
+    const char* ts = getenv("G2M_TIER_STREAMS");
+    const int want_streams = ts ? std::max(1, atoi(ts)) : (K == 5 ? 2 : 1);
+    const bool one_stream = want_streams == 1;
+    const int nstreams = std::min(want_streams, (int)DevState::kSide);
     int nside = 0;
     G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
     auto timed = [&](auto&& fn) -> int {
+        if (!serial && one_stream) {
+            fn(st->stream);
+            G2M_CUDA(cudaGetLastError());
+            return G2M_OK;
+        }
         if (!serial) {
             // ordered after everything on the main stream so far (incl. allocations)
-            cudaStream_t s = st->side[nside % DevState::kSide];
+            cudaStream_t s = st->side[nside % nstreams];
             G2M_CUDA(cudaEventRecord(st->evfork, st->stream));
             G2M_CUDA(cudaStreamWaitEvent(s, st->evfork, 0));
             fn(s);
@@ -1877,7 +1892,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         return G2M_OK;
     };
     auto join = [&]() -> int {
-        for (int i = 0; i < std::min(nside, DevState::kSide); ++i) {
+        for (int i = 0; i < std::min(nside, nstreams); ++i) {
             G2M_CUDA(cudaEventRecord(st->evjoin[i], st->side[i]));
             G2M_CUDA(cudaStreamWaitEvent(st->stream, st->evjoin[i], 0));
         }

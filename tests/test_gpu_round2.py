@@ -161,10 +161,13 @@ def test_cycle4_grid_tier_range_passes(monkeypatch, rng_ids):
     assert got == want
 
 
-def test_concurrent_tiers_equal_serial(monkeypatch):
+@pytest.mark.parametrize("streams", ["1", "2", "8"])
+def test_concurrent_tiers_equal_serial(monkeypatch, streams):
     g = GR.from_edges(G.rmat_edges(14, 16, 1), num_vertices=1 << 14)
     og = pm.orient(g)
+    monkeypatch.setenv("G2M_TIER_STREAMS", streams)
     conc = {k: pm.k_clique(og, k).counts for k in (3, 4, 5)}
+    monkeypatch.delenv("G2M_TIER_STREAMS")
     monkeypatch.setenv("G2M_SERIAL_TIERS", "1")
     og2 = pm.orient(g)
     ser = {k: pm.k_clique(og2, k).counts for k in (3, 4, 5)}
