@@ -149,10 +149,18 @@ def make_graph(spec, device: int, pinned: bool, host: bool = False):
     kind, size = spec
     if kind == "rmat" and size >= 25 and not host:
         # too large for the host generator: R-MAT generated on the device
-        # (same process, device RNG); no host copy (no e2e at this scale)
+        # (same process, device RNG); the e2e leg's host CSR is its pinned
+        # download (the GCSR a user would load)
         g = GR.rmat_device(size, 16, 1, device=device)
-        return g, None, None, {"gen_s": 0.0, "build_s": round(time.perf_counter() - t0, 2),
-                               "generator": "device R-MAT (counter-based RNG)"}
+        info = {"gen_s": 0.0, "build_s": round(time.perf_counter() - t0, 2),
+                "generator": "device R-MAT (counter-based RNG)"}
+        if not pinned:
+            return g, None, None, info
+        import torch
+        po = torch.empty(g.num_vertices + 1, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        pn = torch.empty(g.num_edges, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        g.device_graph(device).download_into(po, pn)
+        return g, po, pn, info
     if kind == "rmat":
         edges, nv = G.rmat_edges(size, 16, 1), 1 << size
     else:
@@ -211,38 +219,38 @@ def api_call(workload, g):
 
 def sample_tasks(gd, tasks, m: int, seed: int):
     """A seeded uniform sample of m tasks of the (implicit) task list:
-    (positions in the list, the tasks as the oracle takes them, edge?)."""
+    (positions in the list or None, the tasks as the oracle takes them,
+    edge?, list length). A reduced edge list (dst < src slots) is sampled by
+    rejection over all slots, so no pass over the whole list is needed; its
+    sample then runs on the GPU as an explicit task list."""
     from paper_2112_09761_b200.graph import EdgeTaskList
     off = np.asarray(gd.row_offsets, dtype=np.int64)
     nbr = gd.neighbors
     edge = isinstance(tasks, EdgeTaskList)
-    if edge and tasks.reduced:
-        # position p of the reduced list = the p-th slot with dst < src
-        lower = np.empty(len(nbr), dtype=bool)
-        nv = gd.num_vertices
-        step = 1 << 20
-        for r0 in range(0, nv, step):
-            r1 = min(nv, r0 + step)
-            s0, s1 = int(off[r0]), int(off[r1])
-            src = np.repeat(np.arange(r0, r1, dtype=np.uint32), np.diff(off[r0:r1 + 1]))
-            lower[s0:s1] = nbr[s0:s1] < src
-        slots = np.flatnonzero(lower)
-        del lower
-    else:
-        slots = None
-    total = len(slots) if slots is not None else (int(off[-1]) if edge else gd.num_vertices)
     rng = np.random.default_rng(seed)
-    pick = np.sort(rng.choice(total, size=min(m, total), replace=False)).astype(np.int64)
     if not edge:
+        total = gd.num_vertices
+        pick = np.sort(rng.choice(total, size=min(m, total), replace=False)).astype(np.int64)
         return pick, pick, False, total
-    s = slots[pick] if slots is not None else pick
-    src = np.searchsorted(off, s, side="right") - 1
-    return pick, np.column_stack([src, nbr[s].astype(np.int64)]), True, total
+    total = len(tasks)
+    slots_all = int(off[-1])
+    if tasks.reduced:
+        if m >= total:      # small graph: the whole reduced list
+            s = np.arange(slots_all, dtype=np.int64)
+        else:
+            s = np.unique(rng.integers(0, slots_all, size=int(m * 2.5) + 64, dtype=np.int64))
+        src = np.searchsorted(off, s, side="right") - 1
+        keep = nbr[s].astype(np.int64) < src
+        s, src = s[keep][:m], src[keep][:m]
+        return None, np.column_stack([src, nbr[s].astype(np.int64)]), True, total
+    pick = np.sort(rng.choice(total, size=min(m, total), replace=False)).astype(np.int64)
+    src = np.searchsorted(off, pick, side="right") - 1
+    return pick, np.column_stack([src, nbr[pick].astype(np.int64)]), True, total
 
 
 def cpu_sample_run(gd, forest, tasks, target_s: float, threads: int, seed: int = 7):
     """Oracle on a seeded uniform sample of the task list; returns
-    (seconds, sampled tasks, total tasks, counts, sample positions)."""
+    (seconds, sampled tasks, total tasks, counts, sample positions, tasks)."""
     from oracle import oracle as O
     m = 2000
     while True:
@@ -251,7 +259,7 @@ def cpu_sample_run(gd, forest, tasks, target_s: float, threads: int, seed: int =
         counts, _ = O.run(gd, forest, tasks=tk, edge=edge, threads=threads)
         dt = time.perf_counter() - t0
         if dt >= target_s * 0.5 or m >= total:
-            return dt, len(tk), total, counts, pick
+            return dt, len(tk), total, counts, pick, tk
         m = int(min(total, m * max(2.0, 0.8 * target_s / max(dt, 1e-3))))
 
 
@@ -450,7 +458,7 @@ def main():
     if args.impl == "reference":
         steps = []
         for i in range(args.warmup + args.steps):
-            dt, m, total, _, _ = cpu_sample_run(gd, forest, tasks, args.cpu_seconds / 4, threads,
+            dt, m, total, _, _, _ = cpu_sample_run(gd, forest, tasks, args.cpu_seconds / 4, threads,
                                                 seed=100 + i)
             if i >= args.warmup:
                 steps.append(dt * total / m)
@@ -639,14 +647,19 @@ def main():
                 "plan_kernel": {k: int(v) for k, v in pc.items()},
                 "equal": {k: int(v) for k, v in pc.items()} == pid_counts}
     if rank == 0 and world == 1 and not (args.no_cpu_baseline and args.no_parity):
-        dt, m, total, ocounts, pick = cpu_sample_run(gd, forest, tasks, args.cpu_seconds, threads)
+        dt, m, total, ocounts, pick, tk_s = cpu_sample_run(gd, forest, tasks, args.cpu_seconds, threads)
         tcpu = dt * total / m
         if not args.no_cpu_baseline:
             cpu = {"value": E / tcpu, "unit": "edges/s", "cores": threads, "kind": "port",
                    "cpu_model": cpu_model(),
                    "sample": f"{m} of {total} tasks (seeded uniform), {dt:.1f}s, extrapolated"}
         if parity is not None:
-            gc, _, _, _ = EX.execute(gd, forest, tasks, device=local, index=pick, lgs=False)
+            if pick is None:    # reduced edge list: the sampled tasks explicitly
+                from paper_2112_09761_b200.graph import EdgeTaskList
+                gc, _, _, _ = EX.execute(gd, forest, EdgeTaskList(tk_s, reduced=True), device=local,
+                                         lgs=False)
+            else:
+                gc, _, _, _ = EX.execute(gd, forest, tasks, device=local, index=pick, lgs=False)
             parity["sample_vs_oracle"] = {
                 "check": "generated plan kernel vs the CPU oracle on the same seeded task sample",
                 "sample_tasks": int(m), "of_tasks": int(total),
