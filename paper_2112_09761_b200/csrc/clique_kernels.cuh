@@ -333,6 +333,174 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
     if (lane == 0 && acc) g2m_add128(count, acc, 0);
 }
 
+// ---------------------------------------------------------------------------
+// staged pair tier (G2M_PAIR_BULK): the pair tier's local-edge tests with
+// the searched lists brought into shared memory by the TMA engine. Row i of
+// A (a = A[i], nk = d-1-i keys A[i+1..d), list L = N+(a) of length l) is
+// *staged* when nk * (ceil log2 l - 4) * 8 >= l, i.e. when its nk global
+// binary searches would fetch more 32-byte sectors (less the ~4 top levels
+// the lanes share in L1) than copying the l * 4 list bytes once: one lane
+// issues a 1-D cp.async.bulk of the list (completion on an mbarrier),
+// double-buffered so the next staged row's copy is in flight while this
+// row's keys are searched in shared memory (~30-cycle LDS steps instead of
+// dependent L2/DRAM round trips). The first copy overlaps the global
+// searches of the unstaged rows (few keys, or lists longer than CAPB - 4).
+// ---------------------------------------------------------------------------
+template <int K, int MAXD, int CAPB>
+struct PairBulkSmem {
+    static constexpr int RW = MAXD > 64 ? 2 : 1;
+    u32 buf[2][CAPB];                   // staged lists, 16-byte aligned
+    u64 R[K > 3 ? MAXD * RW : 2];
+    u64 ro[MAXD];                       // list start of row i
+    u64 bar[2];
+    u32 A[MAXD];
+    u32 rl[MAXD];                       // list length of row i
+    u32 pre[MAXD + 4];                  // exclusive prefix of nk over the global rows
+    u32 grow[MAXD];                     // global-search rows
+    u32 srow[MAXD];                     // staged rows
+};
+
+template <int K, int WPB, int MAXD, int CAPB>
+__global__ void __launch_bounds__(WPB * 32)
+k_clique_pairs_bulk(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
+                    u64 nverts, u64* next, u64 grab, u64* count) {
+    static_assert(K == 3 || MAXD <= 64 || (K == 4 && MAXD <= 128), "row width");
+    static_assert(CAPB % 4 == 0, "16-byte staging buffers");
+    using SM = PairBulkSmem<K, MAXD, CAPB>;
+    constexpr int RW = SM::RW;
+    static_assert(sizeof(SM) % 16 == 0, "per-warp region keeps 16-byte alignment");
+    extern __shared__ __align__(16) unsigned char pb_smem[];
+    SM& S = reinterpret_cast<SM*>(pb_smem)[threadIdx.x >> 5];
+    const u32 lane = g2m_lane();
+    const u32 lt = g2m_lanemask_lt();
+    u32* A = S.A;
+    u64* R = S.R;
+    if (lane == 0) {
+        g2m_mbar_init(&S.bar[0], 1);
+        g2m_mbar_init(&S.bar[1], 1);
+        g2m_fence_barrier_init();
+    }
+    __syncwarp();
+    u32 ph0 = 0, ph1 = 0;     // completed phases per buffer
+    u64 acc = 0;
+    for (;;) {
+        u64 t0 = 0;
+        if (lane == 0) t0 = atomicAdd(next, grab);
+        t0 = __shfl_sync(G2M_FULL, t0, 0);
+        if (t0 >= nverts) break;
+        const u64 t1 = min(t0 + grab, nverts);
+        for (u64 t = t0; t < t1; ++t) {
+            const u32 u = __ldg(verts + t);
+            const u64 b = __ldg(off + u);
+            const u32 d = (u32)(__ldg(off + u + 1) - b);
+            for (u32 x = lane; x < d; x += 32) A[x] = __ldg(nbr + b + x);
+            if constexpr (K > 3)
+                for (u32 x = lane; x < d * RW; x += 32) R[x] = 0;
+            __syncwarp();
+            // classify rows: staged / global-search
+            u32 nst = 0, ng = 0, carry = 0;
+            for (u32 i0 = 0; i0 + 1 < d; i0 += 32) {
+                const u32 i = i0 + lane;
+                const bool valid = i + 1 < d;
+                u64 ro = 0;
+                u32 l = 0, nk = 0;
+                if (valid) {
+                    const u32 a = A[i];
+                    ro = __ldg(off + a);
+                    l = (u32)(__ldg(off + a + 1) - ro);
+                    nk = d - 1 - i;
+                    S.ro[i] = ro;
+                    S.rl[i] = l;
+                }
+                const u32 lg = l > 1 ? 32u - (u32)__clz(l - 1) : 1u;
+                const bool st = valid && l > 0 && l + 4 <= (u32)CAPB && nk * (lg > 4 ? lg - 4 : 1u) * 8u >= l;
+                const bool gl = valid && l > 0 && !st;
+                const u32 ms = __ballot_sync(G2M_FULL, st), mg = __ballot_sync(G2M_FULL, gl);
+                if (st) S.srow[nst + __popc(ms & lt)] = i;
+                const u32 gk = gl ? nk : 0u;
+                const u32 incl = g2m_scan_incl(gk);
+                if (gl) {
+                    const u32 q = ng + __popc(mg & lt);
+                    S.grow[q] = i;
+                    S.pre[q] = carry + incl - gk;
+                }
+                nst += __popc(ms);
+                ng += __popc(mg);
+                carry += __shfl_sync(G2M_FULL, incl, 31);
+            }
+            if (lane == 0) S.pre[ng] = carry;
+            __syncwarp();
+            // first staged copy in flight during the global searches
+            if (nst && lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const u32 i = S.srow[0];
+                g2m_bulk_list(S.buf[0], nbr + S.ro[i], S.rl[i], &S.bar[0]);
+            }
+            // global-search rows: pairs flattened over the lanes
+            for (u32 p = lane; p < carry; p += 32) {
+                u32 lo = 0, n = ng;        // last q with pre[q] <= p
+                while (n > 1) {
+                    const u32 h = n >> 1;
+                    lo = S.pre[lo + h] <= p ? lo + h : lo;
+                    n -= h;
+                }
+                const u32 i = S.grow[lo];
+                const u32 j = i + 1 + (p - S.pre[lo]);
+                if (g2m_has_g(nbr + S.ro[i], S.rl[i], A[j])) {
+                    if constexpr (K == 3) acc += 1;
+                    else atomicOr((u32*)(R + i * RW) + (j >> 5), 1u << (j & 31u));
+                }
+            }
+            // staged rows, double-buffered
+            for (u32 s2 = 0; s2 < nst; ++s2) {
+                const u32 bs = s2 & 1u;
+                if (s2 + 1 < nst && lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const u32 i = S.srow[s2 + 1];
+                    g2m_bulk_list(S.buf[bs ^ 1u], nbr + S.ro[i], S.rl[i], &S.bar[bs ^ 1u]);
+                }
+                g2m_mbar_wait(&S.bar[bs], (bs ? ph1 : ph0) & 1u);
+                if (bs) ++ph1; else ++ph0;
+                const u32 i = S.srow[s2];
+                const u32 l = S.rl[i];
+                const u32* L = S.buf[bs] + (u32)(S.ro[i] & 3ull);
+                for (u32 j = i + 1 + lane; j < d; j += 32) {
+                    if (g2m_has(L, l, A[j])) {
+                        if constexpr (K == 3) acc += 1;
+                        else atomicOr((u32*)(R + i * RW) + (j >> 5), 1u << (j & 31u));
+                    }
+                }
+                __syncwarp();
+            }
+            if constexpr (K > 3 && RW == 1) {
+                __syncwarp();
+                if (lane < d) acc += Chain1<K - 2>::run(R, R[lane]);
+                if (lane + 32 < d) acc += Chain1<K - 2>::run(R, R[lane + 32]);
+            } else if constexpr (K == 4) {
+                __syncwarp();
+                for (u32 i = lane; i < d; i += 32) {
+                    const u64 r0 = R[2 * i], r1 = R[2 * i + 1];
+                    u64 it = r0;
+                    while (it) {
+                        const int j = __ffsll(it) - 1;
+                        it &= it - 1;
+                        acc += (u64)__popcll(r0 & R[2 * j]) + (u64)__popcll(r1 & R[2 * j + 1]);
+                    }
+                    it = r1;
+                    while (it) {
+                        const int j = 64 + __ffsll(it) - 1;
+                        it &= it - 1;
+                        acc += (u64)__popcll(r1 & R[2 * j + 1]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    acc = g2m_wsum(acc);
+    if (lane == 0 && acc) g2m_add128(count, acc, 0);
+}
+
 // Warp-cooperative compaction of the set bits of words[q0, q1) (shared,
 // read by broadcast) into out[] as bit positions; returns the count.
 __device__ __forceinline__ u32 compact_bits(const u64* words, u32 q0, u32 q1, u32* out) {

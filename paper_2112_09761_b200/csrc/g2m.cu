@@ -127,7 +127,9 @@ struct DevBuf {
         release();
         if (n == 0) n = 16;
         s = t_alloc_stream;
-        cudaError_t e = s ? cudaMallocAsync(&p, n, s) : cudaMalloc(&p, n);
+        // +16 B: 1-D bulk copies (g2m_bulk_list) read the 16-byte-aligned
+        // superset of a list, up to 12 bytes past the last element
+        cudaError_t e = s ? cudaMallocAsync(&p, n + 16, s) : cudaMalloc(&p, n + 16);
         if (e != cudaSuccess) {
             cudaGetLastError();
             p = nullptr;
@@ -1971,7 +1973,34 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     G2M_TRY(cta(integral_constant<int, 8>{}, integral_constant<int, 16>{}, F{}, 4, 2));
     G2M_TRY(cta(integral_constant<int, 4>{}, integral_constant<int, 16>{}, F{}, 3, 3));
     G2M_TRY(cta(integral_constant<int, 2>{}, integral_constant<int, 16>{}, F{}, 2, 2));
-    if (kClasses > 8 && sizes[8]) {
+    // G2M_PAIR_BULK=1|2: the staged pair tier (TMA bulk copies of the searched
+    // lists; 1: 2 x 512-element buffers per warp, 2: 2 x 1088)
+    const int pair_bulk = getenv("G2M_PAIR_BULK") ? atoi(getenv("G2M_PAIR_BULK")) : 0;
+    auto bulk_pairs = [&](auto kern, size_t per_warp, int wpb) -> int {
+        const size_t smem = per_warp * wpb;
+        G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        G2M_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem));
+        const u64 grab = std::max<u64>(1, std::min<u64>(16, sizes[8] / ((u64)st->sms * 64 * wpb)));
+        if (dbg)
+            fprintf(stderr, "[g2m] clique k=%d staged pair tier: %llu sources, %zu B smem per warp, %d CTA/SM\n",
+                    K, (unsigned long long)sizes[8], per_warp, occ);
+        G2M_TRY(timed([&](cudaStream_t ss) {
+            ++st->launches;
+            kern<<<st->sms * std::max(occ, 1), wpb * 32, smem, ss>>>(off, nbr, lists + 8 * stride, sizes[8],
+                                                                     next + slot, grab, count);
+        }));
+        ++slot;
+        return G2M_OK;
+    };
+    if (kClasses > 8 && sizes[8] && pair_bulk) {
+        constexpr int WPB = 4;
+        constexpr int MAXD = K == 3 ? 256 : (K == 4 ? 128 : 64);
+        if (pair_bulk == 2)
+            G2M_TRY(bulk_pairs(k_clique_pairs_bulk<K, WPB, MAXD, 1088>, sizeof(PairBulkSmem<K, MAXD, 1088>), WPB));
+        else
+            G2M_TRY(bulk_pairs(k_clique_pairs_bulk<K, WPB, MAXD, 512>, sizeof(PairBulkSmem<K, MAXD, 512>), WPB));
+    } else if (kClasses > 8 && sizes[8]) {
         constexpr int WPB = 8;
         u64 grab = std::max<u64>(1, std::min<u64>(16, sizes[8] / ((u64)st->sms * 64 * WPB)));
         G2M_TRY(timed([&](cudaStream_t ss) {

@@ -524,3 +524,70 @@ __device__ __forceinline__ u32 g2m_hmap_get(const u32* keys, const u32* vals, u3
         h = (h + 1) & mask;
     }
 }
+
+// ---------------------------------------------------------------------------
+// 1-D bulk copies (TMA engine: cp.async.bulk, SASS UBLKCP) global -> shared,
+// completion tracked by a shared-memory mbarrier (transaction bytes).
+// Global source and shared destination must be 16-byte aligned and the size
+// a multiple of 16: g2m_bulk_list copies the 16-byte-aligned superset of a
+// u32 list and returns the list's first element's offset in the copy.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 g2m_smem_addr(const void* p) {
+    return (u32)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void g2m_mbar_init(u64* bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(g2m_smem_addr(bar)), "r"(count) : "memory");
+}
+
+// make initialised barriers visible to the async (TMA) proxy
+__device__ __forceinline__ void g2m_fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// this thread's arrival + the bytes the barrier's phase must also see land
+__device__ __forceinline__ void g2m_mbar_arrive_tx(u64* bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(g2m_smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void g2m_bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            g2m_smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(g2m_smem_addr(bar))
+        : "memory");
+}
+
+// wait for the barrier phase with parity `phase` to complete (all threads
+// that read the copied data call it; try_wait suspends in hardware)
+__device__ __forceinline__ void g2m_mbar_wait(u64* bar, u32 phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W%=;\n}" ::"r"(g2m_smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// Bytes of the aligned copy of list [p, p + n) and the list's offset (u32
+// elements) inside it. 16-byte granules: head = (p & 15) / 4 elements.
+__device__ __forceinline__ u32 g2m_bulk_span(const u32* p, u32 n, u32* head) {
+    const unsigned long long a = (unsigned long long)p;
+    const unsigned long long a0 = a & ~15ull;
+    const unsigned long long a1 = (a + 4ull * n + 15ull) & ~15ull;
+    *head = (u32)((a - a0) >> 2);
+    return (u32)(a1 - a0);
+}
+
+// One thread: arm `bar` with the copy's bytes and issue it; dst must hold
+// g2m_bulk_span bytes (16-byte aligned). Returns the list's offset in dst.
+__device__ __forceinline__ u32 g2m_bulk_list(u32* dst, const u32* p, u32 n, u64* bar) {
+    u32 head;
+    const u32 bytes = g2m_bulk_span(p, n, &head);
+    g2m_mbar_arrive_tx(bar, bytes);
+    g2m_bulk_g2s(dst, (const void*)((unsigned long long)p & ~15ull), bytes, bar);
+    return head;
+}

@@ -1,6 +1,13 @@
-"""Summarise an ncu capture into profiles/: per-kernel table (time, DRAM, L2,
-issue, occupancy, top stalls) and the DRAM bytes per step for bench.py's
-roofline.traffic (profiles/ncu_traffic.json).
+"""Summarise an `ncu --set full` capture of one bench step into profiles/:
+a per-kernel table (time, DRAM bytes and % of peak, L2 % of peak and hit
+rate, issue-active, warps active, warp execution efficiency, top stalls) and
+profiles/ncu_summary.json[key] for bench.py's roofline:
+
+  dram_bytes_per_step   DRAM read + write summed over the captured kernels
+  binding               the dominant kernel's most utilised resource among
+                        DRAM bandwidth, L2 (LTS) throughput and issue slots,
+                        as a fraction of that resource's peak (ncu's own
+                        pct_of_peak_sustained_elapsed / _active)
 
     python scripts/profile_summary.py <rep.ncu-rep> <workload@graph> <out.md>
 """
@@ -16,7 +23,16 @@ rows = list(csv.reader(raw.splitlines()))
 H, U = rows[0], rows[1]
 
 
+def col(*names):
+    for n in names:
+        if n in H:
+            return n
+    return None
+
+
 def val(r, k):
+    if k is None:
+        return float("nan")
     try:
         return float(r[H.index(k)].replace(",", ""))
     except (ValueError, IndexError):
@@ -26,21 +42,36 @@ def val(r, k):
 def scale(k, v):
     u = U[H.index(k)].lower()
     mult = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12,
-            "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
+            "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "s": 1e3, "second": 1e3,
+            "nsecond": 1e-6}
     return v * mult.get(u, 1)
 
 
+K_T = "gpu__time_duration.sum"
+K_DR, K_DW = "dram__bytes_read.sum", "dram__bytes_write.sum"
+K_DPCT = col("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+             "dram__throughput.avg.pct_of_peak_sustained_elapsed")
+K_LPCT = col("lts__throughput.avg.pct_of_peak_sustained_elapsed",
+             "lts__t_sectors.avg.pct_of_peak_sustained_elapsed")
+K_HIT = col("lts__t_sector_hit_rate.pct")
+K_ISS = col("smsp__issue_active.avg.pct_of_peak_sustained_active")
+K_WA = col("sm__warps_active.avg.pct_of_peak_sustained_active")
+K_TE = col("smsp__thread_inst_executed_per_inst_executed.ratio")
+K_L1 = col("l1tex__throughput.avg.pct_of_peak_sustained_active")
 stall_cols = [i for i, h in enumerate(H) if h.startswith("smsp__pcsamp_warps_issue_stalled_")
               and not h.endswith("not_issued")]
+
 lines = [f"# ncu summary: {key} ({Path(rep).name})", "",
-         "| kernel | ms | DRAM read GB | DRAM write GB | L2 hit % | issue active % | warps active % | thread eff | top stalls |",
-         "|---|---|---|---|---|---|---|---|---|"]
-dram_total, ms_total = 0.0, 0.0
+         "`ncu --set full --clock-control none`, one step; per-launch times are serialised and cold-cache "
+         "(compare shares, not absolutes). `warp eff` = threads per warp instruction / 32.", "",
+         "| kernel | ms | DRAM GB (r+w) | DRAM % peak | L2 % peak | L2 hit % | L1 % peak | issue active % | "
+         "warps active % | warp eff % | top stalls |",
+         "|---|---|---|---|---|---|---|---|---|---|---|"]
+kern = []
 for r in rows[2:]:
-    name = r[H.index("Kernel Name")].split("(")[0][:48]
-    ms = scale("gpu__time_duration.sum", val(r, "gpu__time_duration.sum"))
-    rd = scale("dram__bytes_read.sum", val(r, "dram__bytes_read.sum"))
-    wr = scale("dram__bytes_write.sum", val(r, "dram__bytes_write.sum"))
+    name = r[H.index("Kernel Name")].split("(")[0][:56]
+    ms = scale(K_T, val(r, K_T))
+    dram = scale(K_DR, val(r, K_DR)) + scale(K_DW, val(r, K_DW))
     st = []
     for i in stall_cols:
         try:
@@ -50,17 +81,43 @@ for r in rows[2:]:
     st.sort(reverse=True)
     tot = sum(x for x, _ in st) or 1.0
     top = ", ".join(f"{n} {x / tot * 100:.0f}%" for x, n in st[:3])
-    lines.append(f"| {name} | {ms:.2f} | {rd / 1e9:.2f} | {wr / 1e9:.3f} | {val(r, 'lts__t_sector_hit_rate.pct'):.1f} | "
-                 f"{val(r, 'smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} | "
-                 f"{val(r, 'sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | "
-                 f"{val(r, 'smsp__thread_inst_executed_per_inst_executed.ratio'):.1f} | {top} |")
-    if rd == rd and wr == wr:
-        dram_total += rd + wr
-        ms_total += ms
-lines += ["", f"DRAM bytes over the captured kernels: {dram_total / 1e9:.2f} GB in {ms_total:.1f} ms (serialised, cold)."]
+    k = {"name": name, "ms": ms, "dram": dram, "dram_pct": val(r, K_DPCT), "l2_pct": val(r, K_LPCT),
+         "l2_hit": val(r, K_HIT), "l1_pct": val(r, K_L1), "issue": val(r, K_ISS), "warps": val(r, K_WA),
+         "eff": val(r, K_TE) / 32 * 100, "stalls": top}
+    kern.append(k)
+    lines.append(f"| {name} | {ms:.3f} | {dram / 1e9:.3f} | {k['dram_pct']:.1f} | {k['l2_pct']:.1f} | "
+                 f"{k['l2_hit']:.1f} | {k['l1_pct']:.1f} | {k['issue']:.1f} | {k['warps']:.1f} | {k['eff']:.0f} | {top} |")
+
+dram_total = sum(k["dram"] for k in kern if k["dram"] == k["dram"])
+ms_total = sum(k["ms"] for k in kern if k["ms"] == k["ms"])
+# the dominant kernel (name) = most summed time over its launches
+by = {}
+for k in kern:
+    by.setdefault(k["name"], []).append(k)
+dom_name = max(by, key=lambda n: sum(x["ms"] for x in by[n]))
+dk = by[dom_name]
+w = sum(x["ms"] for x in dk) or 1.0
+
+
+def wavg(f):
+    vals = [(x[f], x["ms"]) for x in dk if x[f] == x[f]]
+    return sum(v * t for v, t in vals) / (sum(t for _, t in vals) or 1.0)
+
+
+res = {"dram": wavg("dram_pct") / 100, "l2": wavg("l2_pct") / 100, "issue": wavg("issue") / 100}
+bind = max(res, key=res.get)
+lines += ["",
+          f"DRAM bytes over the captured kernels: {dram_total / 1e9:.3f} GB in {ms_total:.2f} ms (serialised, cold).",
+          f"Dominant kernel: `{dom_name}` ({w:.2f} ms, {w / (ms_total or 1) * 100:.0f}% of the captured time); "
+          f"time-weighted DRAM {res['dram'] * 100:.1f}%, L2 {res['l2'] * 100:.1f}%, issue {res['issue'] * 100:.1f}% "
+          f"of peak -> binding resource: **{bind}**."]
 out.write_text("\n".join(lines) + "\n")
-tj = Path("profiles/ncu_traffic.json")
-d = json.loads(tj.read_text()) if tj.exists() else {}
-d[key] = {"dram_bytes_per_step": int(dram_total), "source": f"{out} (ncu --set full, one step, sum over kernels)"}
-tj.write_text(json.dumps(d, indent=1) + "\n")
+sj = Path("profiles/ncu_summary.json")
+d = json.loads(sj.read_text()) if sj.exists() else {}
+d[key] = {"dram_bytes_per_step": int(dram_total), "captured_ms": ms_total,
+          "binding": {"kernel": dom_name, "resource": bind, "frac": res[bind],
+                      "dram_frac": res["dram"], "l2_frac": res["l2"], "issue_frac": res["issue"],
+                      "warp_exec_eff": wavg("eff") / 100},
+          "source": f"{out} (ncu --set full, one step, sum over kernels)"}
+sj.write_text(json.dumps(d, indent=1, sort_keys=True) + "\n")
 print("\n".join(lines))

@@ -218,3 +218,18 @@ def test_rmat22_pinned_counts():
     assert g.num_edges // 2 == 64_153_257
     assert pm.triangle_count(g) == 2_111_865_705
     assert pm.k_clique(g, 4).counts == {"4-clique": 124_164_530_433}
+
+
+@pytest.mark.parametrize("bulk", ["1", "2"])
+def test_staged_pair_tier_matches_plan_kernel(monkeypatch, bulk):
+    # the TMA-staged pair tier (cp.async.bulk + mbarrier) against the generated
+    # plan kernel; RMAT-15 puts most sources in the pair tier
+    g = GR.from_edges(G.rmat_edges(15, 16, 5), num_vertices=1 << 15)
+    og = pm.orient(g)
+    monkeypatch.setenv("G2M_PAIR_BULK", bulk)
+    for k in (3, 4, 5):
+        f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
+        tasks = EX._default_tasks(og, f)
+        got = EX.execute(og, f, tasks)[0]
+        want = EX.execute(og, f, tasks, lgs=False)[0]
+        assert got == want, (k, got, want)
