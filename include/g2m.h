@@ -58,7 +58,7 @@
 extern "C" {
 #endif
 
-#define G2M_ABI_VERSION 4
+#define G2M_ABI_VERSION 5
 
 #define G2M_OK 0
 #define G2M_EUSAGE 1
@@ -198,6 +198,15 @@ int g2m_kernel_work(const g2m_graph* g, int32_t family, uint64_t* out);
 /* len(EdgeTaskList.implicit(g, reduced=True)) (graph.py:270-286): slots with
  * dst < src, counted on the device (cached with the reduced task offsets). */
 int g2m_graph_reduced_tasks(const g2m_graph* g, uint64_t* out);
+/* Hub-pattern vertex partition (replaces scheduler.partition_vertices_for_hub,
+ * scheduler.py:125-163): the owned range [lo, hi) plus its 1-hop closure as
+ * the induced subgraph, ids renamed in ascending global order, built on the
+ * device. *num_local = its vertex count; the owned vertices are the local
+ * ids [*first_owned, *first_owned + hi - lo). g2m_graph_local_ids copies the
+ * local -> global map (num_local u32) of such a part. */
+int g2m_graph_hub_part(const g2m_graph* g, uint64_t lo, uint64_t hi, g2m_graph** out,
+                       uint64_t* num_local, uint64_t* first_owned);
+int g2m_graph_local_ids(const g2m_graph* g, uint32_t* local_to_global);
 
 int g2m_kernel_compile(const char* cuda_source, const char* kernel_name,
                        const char* const* header_sources, const char* const* header_names,

@@ -233,6 +233,10 @@ struct g2m_graph {
     DevBuf wpre;
     int wpre_key = -1;
     uint64_t wpre_total = 0, wpre_sources = 0;
+    // hub partitions (g2m_graph_hub_part): local -> global ids, and the local
+    // id of the first owned vertex (owned vertices are consecutive)
+    DevBuf l2g;
+    uint64_t part_first = 0, part_owned = 0;
 };
 
 // out[0] = max degree, out[1] = Σ degree² (the BFS frontier bound, executor.choose_search)
@@ -611,6 +615,155 @@ extern "C" int g2m_graph_orient(const g2m_graph* g, g2m_graph** out) {
     std::lock_guard<std::mutex> lk(st->mu);
     G2M_CUDA(cudaSetDevice(g->dev));
     return orient_impl(g, st, out);
+}
+
+// ---- hub-pattern vertex partitioning (scheduler.py:125-163)
+// Part [lo, hi) of the vertex range plus its 1-hop closure, as the induced
+// subgraph with ids renamed in ascending global order: every search rooted
+// at an owned vertex of a hub pattern (all others adjacent to the root)
+// stays inside the part. Built on the device: mark, scan, gather rows.
+
+__global__ void k_hub_mark(const u64* off, const u32* nbr, u64 lo, u64 hi, u32* flag) {
+    const u64 s0 = off[lo], s1 = off[hi];
+    for (u64 v = lo + blockIdx.x * (u64)blockDim.x + threadIdx.x; v < hi; v += (u64)gridDim.x * blockDim.x)
+        flag[v] = 1u;
+    for (u64 s = s0 + blockIdx.x * (u64)blockDim.x + threadIdx.x; s < s1; s += (u64)gridDim.x * blockDim.x)
+        flag[nbr[s]] = 1u;
+}
+
+// g2l = exclusive scan of flag (u64); l2g[g2l[v]] = v for flagged v
+__global__ void k_hub_l2g(const u32* flag, const u64* g2l, u64 nv, u32* l2g) {
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x)
+        if (flag[v]) l2g[g2l[v]] = (u32)v;
+}
+
+// one warp per local vertex: kept neighbours (count pass) or their local ids
+// in order (fill pass, ballot compaction)
+template <bool FILL>
+__global__ void k_hub_rows(const u64* off, const u32* nbr, const u32* flag, const u64* g2l, const u32* l2g,
+                           u64 nsub, u64* cnt, const u64* soff, u32* snbr) {
+    const u32 lane = g2m_lane();
+    for (u64 x = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; x < nsub;
+         x += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u32 v = l2g[x];
+        const u64 b = off[v], e = off[v + 1];
+        u64 pos = FILL ? soff[x] : 0;
+        u64 c = 0;
+        for (u64 s0 = b; s0 < e; s0 += 32) {
+            const u64 s = s0 + lane;
+            u32 w = 0;
+            bool keep = false;
+            if (s < e) {
+                w = nbr[s];
+                keep = flag[w] != 0u;
+            }
+            const u32 m = __ballot_sync(G2M_FULL, keep);
+            if (FILL && keep) snbr[pos + __popc(m & g2m_lanemask_lt())] = (u32)g2l[w];
+            pos += __popc(m);
+            c += __popc(m);
+        }
+        if (!FILL && lane == 0) cnt[x] = c;
+    }
+}
+
+__global__ void k_gather_u32(const u32* src, const u32* idx, u64 n, u32* dst) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+__global__ void k_u32_to_u64(const u32* a, u64 n, u64* b) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
+extern "C" int g2m_graph_hub_part(const g2m_graph* g, uint64_t lo, uint64_t hi, g2m_graph** out,
+                                  uint64_t* num_local, uint64_t* first_owned) {
+    if (!g || !out || !num_local || !first_owned) return fail(G2M_EUSAGE, "null argument");
+    if (lo > hi || hi > g->nv) return fail(G2M_EUSAGE, "owned range outside the vertex range");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    const u64 nv = g->nv;
+    auto o = std::make_unique<g2m_graph>();
+    o->dev = g->dev;
+    o->oriented = g->oriented;
+    DevBuf flag, flag64, g2l, cnt;
+    G2M_TRY(flag.ensure(std::max<u64>(nv, 1) * 4));
+    G2M_TRY(flag64.ensure(std::max<u64>(nv, 1) * 8));
+    G2M_TRY(g2l.ensure((nv + 1) * 8));
+    G2M_CUDA(cudaMemsetAsync(flag.p, 0, std::max<u64>(nv, 1) * 4, st->stream));
+    if (hi > lo) {
+        ++st->launches;
+        k_hub_mark<<<grid_for(st, std::max<u64>(hi - lo, 1) * 8, 256), 256, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), lo, hi, flag.as<u32>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    if (nv) {
+        ++st->launches;
+        k_u32_to_u64<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(flag.as<u32>(), nv, flag64.as<u64>());
+    }
+    G2M_TRY(exclusive_scan_u64(st, flag64.as<u64>(), g2l.as<u64>(), nv));
+    u64 nsub = 0;
+    G2M_CUDA(cudaMemcpyAsync(&nsub, g2l.as<u64>() + nv, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    o->nv = nsub;
+    G2M_TRY(o->l2g.ensure(std::max<u64>(nsub, 1) * 4));
+    G2M_TRY(o->off.ensure((nsub + 1) * 8));
+    G2M_TRY(cnt.ensure(std::max<u64>(nsub, 1) * 8));
+    if (nv) {
+        ++st->launches;
+        k_hub_l2g<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(flag.as<u32>(), g2l.as<u64>(), nv, o->l2g.as<u32>());
+    }
+    if (nsub) {
+        ++st->launches;
+        k_hub_rows<false><<<grid_for(st, nsub * 32, 256), 256, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), flag.as<u32>(), g2l.as<u64>(), o->l2g.as<u32>(), nsub,
+            cnt.as<u64>(), nullptr, nullptr);
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), o->off.as<u64>(), nsub));
+    G2M_CUDA(cudaMemcpyAsync(&o->slots, o->off.as<u64>() + nsub, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    G2M_TRY(o->nbr.ensure(std::max<u64>(o->slots, 1) * 4));
+    if (nsub) {
+        ++st->launches;
+        k_hub_rows<true><<<grid_for(st, nsub * 32, 256), 256, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), flag.as<u32>(), g2l.as<u64>(), o->l2g.as<u32>(), nsub, nullptr,
+            o->off.as<u64>(), o->nbr.as<u32>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    if (g->labels.p) {
+        G2M_TRY(o->labels.ensure(std::max<u64>(nsub, 1) * 4));
+        if (nsub) {
+            ++st->launches;
+            k_gather_u32<<<grid_for(st, nsub, 256), 256, 0, st->stream>>>(g->labels.as<u32>(), o->l2g.as<u32>(),
+                                                                          nsub, o->labels.as<u32>());
+        }
+    }
+    u64 first = 0;
+    if (hi > lo) G2M_CUDA(cudaMemcpyAsync(&first, g2l.as<u64>() + lo, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    G2M_TRY(finish_graph(o.get(), st));
+    o->part_first = first;
+    o->part_owned = hi - lo;
+    *num_local = nsub;
+    *first_owned = first;
+    *out = o.release();
+    return G2M_OK;
+}
+
+extern "C" int g2m_graph_local_ids(const g2m_graph* g, uint32_t* local_to_global) {
+    if (!g || !local_to_global) return fail(G2M_EUSAGE, "null argument");
+    if (!g->l2g.p) return fail(G2M_EUSAGE, "graph is not a hub partition");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    if (g->nv)
+        G2M_CUDA(cudaMemcpyAsync(local_to_global, g->l2g.p, g->nv * 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return G2M_OK;
 }
 
 extern "C" int g2m_graph_replicate(const g2m_graph* g, int32_t device, g2m_graph** out) {

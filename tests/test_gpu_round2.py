@@ -233,3 +233,53 @@ def test_staged_pair_tier_matches_plan_kernel(monkeypatch, bulk):
         got = EX.execute(og, f, tasks)[0]
         want = EX.execute(og, f, tasks, lgs=False)[0]
         assert got == want, (k, got, want)
+
+
+@pytest.mark.parametrize("w", ["tc", "4-cycle", "3-motif"])
+def test_least_first_schedule_counts(w):
+    # chunked least-first queues (explicit task indices) over 4 parts folded
+    # onto the GPU: counts equal the one-device run
+    g = GR.from_edges(G.powerlaw_edges(3000, 4, 3), num_vertices=3000)
+    pats = {"tc": [P.generate_clique(3)], "4-cycle": [cycle4()], "3-motif": P.generate_all_motifs(3)}[w]
+    one = pm.run_job(pm.MiningJob(graph=g, patterns=pats, mode="count"))
+    four = pm.run_job(pm.MiningJob(graph=g, patterns=pats, mode="count", devices=4,
+                                   policy=scheduler.POLICY_LEAST))
+    assert four.counts == one.counts
+    assert len(four.devices.reports) == 4
+
+
+def _host_hub_parts(g, n):
+    """Host restatement of the reference's partition_vertices_for_hub
+    (scheduler.py:125-163): owned range + 1-hop closure, induced subgraph."""
+    off = g.row_offsets.astype(np.int64)
+    nbr = g.neighbors.astype(np.int64)
+    nv = g.num_vertices
+    q, r = divmod(nv, n)
+    out, start = [], 0
+    for i in range(n):
+        size = q + (1 if i < r else 0)
+        owned = np.arange(start, start + size)
+        start += size
+        verts = np.unique(np.concatenate([owned, nbr[off[start - size]:off[start]]])) if size else owned
+        g2l = np.full(nv, -1)
+        g2l[verts] = np.arange(len(verts))
+        rows = [g2l[nbr[off[v]:off[v + 1]]] for v in verts]
+        rows = [x[x >= 0] for x in rows]
+        so = np.zeros(len(verts) + 1, dtype=np.uint64)
+        np.cumsum([len(x) for x in rows], out=so[1:])
+        sn = np.concatenate(rows).astype(np.uint32) if rows else np.empty(0, np.uint32)
+        out.append((so, sn, g2l[owned], verts))
+    return out
+
+
+@pytest.mark.parametrize("n", [1, 3, 7])
+def test_device_hub_partition_equals_reference_restatement(n):
+    g = GR.from_edges(G.rmat_edges(10, 8, 6), num_vertices=1 << 10, labels=np.arange(1 << 10) % 5)
+    pl = make_plan(P.generate_clique(4), g, granularity="vertex")
+    parts = scheduler.partition_vertices_for_hub(g, n, pl)
+    for part, (so, sn, owned, verts) in zip(parts, _host_hub_parts(g, n)):
+        assert np.array_equal(part.subgraph.row_offsets, so)
+        assert np.array_equal(part.subgraph.neighbors, sn)
+        assert np.array_equal(part.owned_local, owned)
+        assert np.array_equal(part.local_to_global, verts)
+        assert np.array_equal(part.subgraph.labels, g.labels[verts])
