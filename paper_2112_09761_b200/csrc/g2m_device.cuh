@@ -358,6 +358,16 @@ __device__ __forceinline__ u32 g2m_scan_incl(u32 x) {
     return x;
 }
 
+__device__ __forceinline__ u64 g2m_scan_incl64(u64 x) {
+    const u32 lane = g2m_lane();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u64 y = __shfl_up_sync(G2M_FULL, x, o);
+        if (lane >= (u32)o) x += y;
+    }
+    return x;
+}
+
 // ---------------------------------------------------------------------------
 // Instrumentation: SURVEY.md 8(d) algorithmic bytes of the REFERENCE plan
 // (4*(|a|+|b|) per set op as the reference executor passes its operands,

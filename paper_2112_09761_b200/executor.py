@@ -22,7 +22,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _native as N
-from . import codegen
+from . import codegen, codegen_lgs
 from .graph import EdgeTaskList, Graph, build_edge_tasks
 from .pattern import EDGE_INDUCED
 from .plan import (EDGE_PARALLEL, EMIT_MATCH, VERTEX_PARALLEL, PlanForest,
@@ -156,6 +156,10 @@ def compile_forest(forest: PlanForest, labeled: bool, list_mode: bool, max_degre
                            smem_slot_cap=cap, warps_per_block=WARPS_PER_BLOCK,
                            stage_words=STAGE_WORDS, flatten=flatten, instrument=instrument,
                            frontier=frontier)
+    return _compile_gen(gen, instrument)
+
+
+def _compile_gen(gen: codegen.GeneratedKernel, instrument: bool) -> CompiledPlan:
     key = gen.key
     with _cache_lock:
         hit = _cache.get(key)
@@ -262,6 +266,9 @@ def _counts_from(words: np.ndarray, pids) -> dict[str, int]:
 # k values routed to the bitmap local-graph clique kernels (g2m_clique_count);
 # G2M_TC_LGS=0 sends triangle counting to the generated plan kernel instead
 LGS_CLIQUE_K = {3, 4, 5}
+# G2M_LGS_GENERATED=1: run_dfs_lgs sends k-clique counts to the generated
+# LGS kernel too (tests compare it with the hand-written tiers)
+LGS_GENERATED_CLIQUES = os.environ.get("G2M_LGS_GENERATED") == "1"
 if os.environ.get("G2M_TC_LGS") == "0":
     LGS_CLIQUE_K.discard(3)
 
@@ -516,6 +523,14 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
     list_mode = sink is not None and _has_emitters(forest)
     cp = compile_forest(forest, labeled, list_mode, dg.max_degree, flatten=flatten,
                         instrument=instrument)
+    return _run_kernel(cp, dg, forest, tasks, sink, list_mode, rr=rr, index=index,
+                       run_config=run_config)
+
+
+def _run_kernel(cp: "CompiledPlan", dg, forest: PlanForest, tasks, sink, list_mode: bool,
+                rr=None, index=None, run_config: N.RunConfig | None = None):
+    """g2m_run (count) or g2m_list (matches to ``sink`` in the reference's
+    order) of a compiled kernel; returns (counts, RunStats, stopped, cp)."""
     spec, keep = task_spec(tasks, rr=rr, index=index)
     words = np.zeros(2 * max(cp.gen.num_patterns, 1), dtype=np.uint64)
     stats = N.RunStats()
@@ -551,6 +566,13 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
         stopped = N.check(rc, "list") == N.G2M_STOPPED
     del keep
     return _counts_from(words, cp.gen.pattern_ids), stats, stopped, cp
+
+
+def compile_lgs(plan: SearchPlan, list_mode: bool, max_degree: int) -> CompiledPlan:
+    """Generate + NVRTC-compile the bitmap local-graph-search kernel of a
+    hub-rooted plan (codegen_lgs; cached by generated source)."""
+    gen = codegen_lgs.generate_lgs(plan, list_mode=list_mode, max_degree=max_degree)
+    return _compile_gen(gen, instrument=False)
 
 
 # ---------------------------------------------------------------------------
@@ -626,11 +648,22 @@ def run_dfs_lgs(g: Graph, plan: SearchPlan, tasks=None,
         anchored = 1
     if anchored + 1 > plan.depth:
         raise ValueError("plan too shallow for local graph search")
+    codegen_lgs.check_plan(plan)
     num_tasks = len(tasks)
     workers = resolve_worker_count(cfg, plan.num_buffers, g.max_degree, num_tasks)
     t0 = time.perf_counter()
     forest = as_forest(plan)
-    counts, st, stopped, _ = execute(g, forest, tasks, sink=sink, device=device)
+    if _lgs_clique_k(g, forest, tasks, sink, None) and not LGS_GENERATED_CLIQUES:
+        # k-clique counts: the hand-written bitmap LGS tiers (g2m_clique_count)
+        counts, st, stopped, _ = execute(g, forest, tasks, sink=sink, device=device)
+    else:
+        # every other hub-rooted plan: the generated bitmap LGS kernel
+        dev = N.default_device() if device is None else device
+        N.require_device(dev)
+        dg = g.device_graph(dev)
+        list_mode = sink is not None and _has_emitters(forest)
+        cp = compile_lgs(plan, list_mode, dg.max_degree)
+        counts, st, stopped, _ = _run_kernel(cp, dg, forest, tasks, sink, list_mode)
     counts = {plan.pattern_id: counts.get(plan.pattern_id, 0)}
     high = tuple(int(st.high_water[i]) if i < 8 else 0 for i in range(plan.num_buffers))
     stats = ExecStats(workers=workers, tasks=num_tasks, num_buffers=plan.num_buffers,
