@@ -124,9 +124,9 @@ class _LgsGen:
         o = self.o
         for l in range(1, level):
             if l in self.anch:
-                o(f"if (in{l}) {dst}[p{l} >> 6] &= ~(1ull << (p{l} & 63u));")
+                o(f"if (in{l}) g2m_lgs_clear({dst}, p{l});")
             else:
-                o(f"{dst}[l{l} >> 6] &= ~(1ull << (l{l} & 63u));")
+                o(f"g2m_lgs_clear({dst}, l{l});")
 
     def cutoff(self, lv) -> str:
         b = lv.bound
@@ -172,7 +172,7 @@ class _LgsGen:
         else:
             o("#pragma unroll 1")
             o.push("for (int q = 0; q < W; ++q) {")
-            o(f"u64 bits = s{L}[q];")
+            o(f"u64 bits = g2m_lgs_get(s{L}, q);")
             o.push("while (bits) {")
             o(f"const u32 l{L} = (u32)q * 64u + (u32)(__ffsll((long long)bits) - 1);")
             o("bits &= bits - 1;")
@@ -220,19 +220,35 @@ class _LgsGen:
         w("    for (int q = 0; q < NW; ++q) c += (u64)__popcll(v[q]);")
         w("    return c;")
         w("}")
+        w("// word q / clear bit b of a W-word set held in registers (unrolled selects:")
+        w("// a dynamic index would move the array to local memory)")
+        w("__device__ __forceinline__ u64 g2m_lgs_get(const u64 (&v)[W], int q) {")
+        w("    u64 r = 0;")
+        w("#pragma unroll")
+        w("    for (int i = 0; i < W; ++i) r = i == q ? v[i] : r;")
+        w("    return r;")
+        w("}")
+        w("__device__ __forceinline__ void g2m_lgs_clear(u64 (&v)[W], u32 b) {")
+        w("#pragma unroll")
+        w("    for (int i = 0; i < W; ++i) if ((u32)i == (b >> 6)) v[i] &= ~(1ull << (b & 63u));")
+        w("}")
         w("// i-th set bit (0-based) of v[W]")
         w("__device__ __forceinline__ u32 g2m_lgs_nth(const u64 (&v)[W], u32 i) {")
-        w("#pragma unroll 1")
+        w("    u32 res = 0u;")
+        w("    bool done = false;")
+        w("#pragma unroll")
         w("    for (int q = 0; q < W; ++q) {")
         w("        const u32 pc = (u32)__popcll(v[q]);")
-        w("        if (i < pc) {")
+        w("        if (!done && i < pc) {")
         w("            u64 b = v[q];")
         w("            for (u32 r = 0; r < i; ++r) b &= b - 1;")
-        w("            return (u32)q * 64u + (u32)(__ffsll((long long)b) - 1);")
+        w("            res = (u32)q * 64u + (u32)(__ffsll((long long)b) - 1);")
+        w("            done = true;")
+        w("        } else if (!done) {")
+        w("            i -= pc;")
         w("        }")
-        w("        i -= pc;")
         w("    }")
-        w("    return 0u;")
+        w("    return res;")
         w("}")
         w(f'extern "C" __global__ void __launch_bounds__(WPB * 32) {KERNEL_NAME}(const G2MArgs a) {{')
         w("    extern __shared__ __align__(16) u32 g2m_smem[];")
