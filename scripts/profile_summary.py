@@ -9,7 +9,7 @@ profiles/ncu_summary.json[key] for bench.py's roofline:
                         as a fraction of that resource's peak (ncu's own
                         pct_of_peak_sustained_elapsed / _active)
 
-    python scripts/profile_summary.py <rep.ncu-rep> <workload@graph> <out.md>
+    python scripts/profile_summary.py <rep.ncu-rep> <workload@graph> <out.md> [summary.json]
 """
 import csv
 import json
@@ -112,7 +112,7 @@ lines += ["",
           f"time-weighted DRAM {res['dram'] * 100:.1f}%, L2 {res['l2'] * 100:.1f}%, issue {res['issue'] * 100:.1f}% "
           f"of peak -> binding resource: **{bind}**."]
 out.write_text("\n".join(lines) + "\n")
-sj = Path("profiles/ncu_summary.json")
+sj = Path(sys.argv[4] if len(sys.argv) > 4 else "profiles/ncu_summary.json")
 d = json.loads(sj.read_text()) if sj.exists() else {}
 d[key] = {"dram_bytes_per_step": int(dram_total), "captured_ms": ms_total,
           "binding": {"kernel": dom_name, "resource": bind, "frac": res[bind],
