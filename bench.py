@@ -676,6 +676,10 @@ def main():
         sim = {}
         P = args.simulate_parts
         splits = [("est", EX.SOURCE_CHUNK), ("rr", 1)] if family in ("lgs", "cycle4") else [(None, None)]
+        if family in ("lgs", "cycle4") and os.environ.get("G2M_SIM_SPLITS"):
+            # e.g. "est:1,est:16,rr:1": every listed source split in one process
+            splits = [(a, int(b or 1)) for a, _, b in
+                      (x.partition(":") for x in os.environ["G2M_SIM_SPLITS"].split(","))]
         for split, chunk in splits:
             part_ms, tot = [], {}
             for i in range(P):

@@ -1,0 +1,12 @@
+# round 2: compute-sanitizer (memcheck, racecheck, synccheck) on the small workload, the
+# multi-GPU split simulations (estimator chunk sizes vs one-by-one), then the ncu sweep
+mkdir -p gpurun_out
+T=${1:-r02f}
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_workload.py 10 > gpurun_out/${T}_sanitize_${tool}.log 2>&1; echo $tool rc=$?; grep -E "ERROR SUMMARY|MISMATCHES|Error" gpurun_out/${T}_sanitize_${tool}.log | head -5
+done
+for w in cl4 tc c4; do
+  G2M_SIM_SPLITS=est:1,est:16,est:64,est:256,rr:1 timeout 1200 python bench.py --workload $w --steps 1 --warmup 1 --simulate-parts 8 --no-cpu-baseline --no-e2e --no-parity --no-roofline > gpurun_out/${T}_sim_${w}.json 2> gpurun_out/${T}_sim_${w}.err
+  echo $w rc=$?; grep "simulated split" gpurun_out/${T}_sim_${w}.err
+done
+bash scripts/gpu_ncu_r02.sh r02n "cl4 tc cl5 tc:G2M_PAIR_BULK=1 c4 diamond mc3 mc4 tc27"
