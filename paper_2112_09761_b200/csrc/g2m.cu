@@ -175,6 +175,16 @@ struct DevState {
 static std::mutex g_dev_mu;
 static std::map<int, std::unique_ptr<DevState>> g_devs;
 
+// Grow-only scratch of the O(E) preprocessing passes (graph build, rank
+// relabelling) can reach tens of GB at RMAT-27 (a radix sort of 4.3e9 keys):
+// hand it back to the pool once the pass is done.
+static void trim_scratch(DevState* st) {
+    const size_t big = (size_t)1 << 30;
+    if (st->cub_tmp.bytes > big) st->cub_tmp.release();
+    if (st->tmp1.bytes > big) st->tmp1.release();
+    if (st->tmp2.bytes > big) st->tmp2.release();
+}
+
 static int dev_state(int dev, DevState** out) {
     std::lock_guard<std::mutex> lk(g_dev_mu);
     auto it = g_devs.find(dev);
@@ -906,6 +916,7 @@ static int keys_to_graph(DevState* st, int device, uint64_t n, DevBuf& keys, Dev
         if (n) G2M_CUDA(cudaMemcpyAsync(g->labels.p, labels, n * 4, cudaMemcpyHostToDevice, st->stream));
     }
     G2M_TRY(finish_graph(g.get(), st));
+    trim_scratch(st);
     *out = g.release();
     return G2M_OK;
 }
@@ -1274,6 +1285,7 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     }
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     phase("rows");
+    trim_scratch(st);
     g->has_rank = true;
     return G2M_OK;
 }

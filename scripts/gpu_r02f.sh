@@ -9,4 +9,3 @@ for w in cl4 tc c4; do
   G2M_SIM_SPLITS=est:1,est:16,est:64,est:256,rr:1 timeout 1200 python bench.py --workload $w --steps 1 --warmup 1 --simulate-parts 8 --no-cpu-baseline --no-e2e --no-parity --no-roofline > gpurun_out/${T}_sim_${w}.json 2> gpurun_out/${T}_sim_${w}.err
   echo $w rc=$?; grep "simulated split" gpurun_out/${T}_sim_${w}.err
 done
-bash scripts/gpu_ncu_r02.sh r02n "cl4 tc cl5 tc:G2M_PAIR_BULK=1 c4 diamond mc3 mc4 tc27"
