@@ -39,10 +39,10 @@ for w in works:
         for k, v in kv:
             os.environ[k] = v
         ms = []
-        for i in range(6):
+        for i in range(int(os.environ.get("AB_REPS", "6"))):
             c, st, _, _ = EX.execute(pj.graph, pj.forest, pj.tasks)
             ms.append(st.kernel_ms)
-        print(f"{w} [{s}] kernel_ms {np.round(ms, 2).tolist()} min {min(ms[1:]):.2f} mean {np.mean(ms[1:]):.2f} counts {c}",
+        print(f"{w} [{s}] kernel_ms {np.round(ms, 2).tolist()} min {min(ms[1:] or ms):.2f} mean {np.mean(ms[1:] or ms):.2f} counts {c}",
               flush=True)
         if debug:
             os.environ["G2M_DEBUG"] = "1"

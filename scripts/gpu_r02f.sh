@@ -9,3 +9,6 @@ for w in cl4 tc c4; do
   G2M_SIM_SPLITS=est:1,est:16,est:64,est:256,rr:1 timeout 1200 python bench.py --workload $w --steps 1 --warmup 1 --simulate-parts 8 --no-cpu-baseline --no-e2e --no-parity --no-roofline > gpurun_out/${T}_sim_${w}.json 2> gpurun_out/${T}_sim_${w}.err
   echo $w rc=$?; grep "simulated split" gpurun_out/${T}_sim_${w}.err
 done
+# 4-cycle tier breakdown at RMAT-25 and RMAT-27 (G2M_DEBUG per-tier times)
+AB_REPS=1 timeout 900 python scripts/ab_env.py 25 c4 "X=0" debug > gpurun_out/${T}_c425_tiers.txt 2>&1; echo c425 rc=$?; grep -E "cycle4|c4 " gpurun_out/${T}_c425_tiers.txt | head -20
+AB_REPS=1 timeout 1200 python scripts/ab_env.py 27 c4 "X=0" debug > gpurun_out/${T}_c427_tiers.txt 2>&1; echo c427 rc=$?; grep -E "cycle4|c4 " gpurun_out/${T}_c427_tiers.txt | head -20
