@@ -647,6 +647,11 @@ __device__ __forceinline__ u32 cta_probe(const u64* __restrict__ off, const u32*
 // compacted again and shared by the whole warp.
 // bmw: u32 words of the window bitmap (0 = hash only).
 // ---------------------------------------------------------------------------
+// k = 5: local sources i with 128 < |R_i| <= 256 deferred to a CTA-wide phase
+// that compresses R_i's sub-DAG to 4-word rows (set by the host per launch;
+// G2M_CL5_BIG=0 keeps them on the per-warp W-word path).
+__device__ u32 g_cl5_big = 1;
+
 // Blocks per SM the narrow tiers are launched at (g2m.cu): keeps the register
 // budget at what that occupancy allows (the window/hash variants add live values).
 __host__ __device__ constexpr int cta_min_blocks(int K, int W) {
@@ -682,13 +687,14 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
     u32* L2 = L1 + 256;
     u64* t2s = T + w * (W + 1);
     __shared__ u64 s_u;
-    __shared__ u32 s_cnt, s_tot, s_nlong, s_lrow, s_flat;
+    __shared__ u32 s_cnt, s_tot, s_nlong, s_lrow, s_flat, s_nbig, s_n1;
     for (u32 x = threadIdx.x; x < bmw; x += NW * 32) BM[x] = 0;
     u64 acc = 0;
     for (;;) {
         if (threadIdx.x == 0) {
             s_u = atomicAdd(next, 1ull);
             s_cnt = 0;
+            s_nbig = 0;
             s_nlong = 0;
             s_lrow = 0;
             s_flat = 0;
@@ -850,6 +856,11 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                     // R_i. With n1 = |R_i| <= 128 its rows fit two words:
                     // S_k bit m <=> L1[m] in R_{L1[k]}, four ballots per k.
                     const u32 n1 = __reduce_add_sync(G2M_FULL, (u32)__popcll(myw));
+                    if (n1 > 128 && n1 <= 256 && W >= 4 && g_cl5_big) {
+                        // CTA-wide compressed phase below (LR is free after the probe)
+                        if (lane == 0) LR[atomicAdd(&s_nbig, 1u)] = i;
+                        continue;
+                    }
                     if (n1 <= 128) {
                         // sub-DAG rows of up to 128 bits (two words): lane q*32+l holds
                         // candidate c[q]; S_k = ballots of "c in R_{L1[k]}"
@@ -966,6 +977,59 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                     }
                     __syncwarp();
                 }
+                }
+            }
+            if constexpr (K == 5 && W >= 4) {
+                // Deferred rows (128 < |R_i| <= 256): the whole CTA compresses R_i's
+                // sub-DAG to 4-word rows S_k (bit m <=> CS[m] in R_{CS[k]}, 8 ballots
+                // per k), then counts its triangles warp-per-k, lanes over the set bits
+                // of S_k: 4 words per (k, l) instead of W per (j, l) on the per-warp path.
+                // The union region is free once every warp has left the row loop.
+                __syncthreads();
+                const u32 nbig = s_nbig;
+                u64* SS = (u64*)scr;                    // [256][4] u64
+                u32* CS = scr + 2048;                   // [256] candidates of R_i
+                u32* LW = CS + 256 + w * 256;           // per-warp set-bit list
+                for (u32 bi = 0; bi < nbig; ++bi) {
+                    const u32 i = LR[bi];
+                    if (w == 0) {
+                        const u32 n1 = compact_bits(R + (u64)i * Ws, 0, Wd, CS);
+                        if (lane == 0) s_n1 = n1;
+                    }
+                    __syncthreads();
+                    const u32 n1 = s_n1;
+                    const u32 ng = (n1 + 31) >> 5;
+                    for (u32 k = w; k < n1; k += NW) {
+                        const u64* Rk = R + (u64)CS[k] * Ws;
+                        u32 sw[8];
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) {
+                            const u32 m = (u32)g * 32u + lane;
+                            const bool bq = (u32)g < ng && (u32)g >= (k >> 5) && m < n1 &&
+                                            ((Rk[CS[m] >> 6] >> (CS[m] & 63u)) & 1ull);
+                            sw[g] = __ballot_sync(G2M_FULL, bq);
+                        }
+                        if (lane == 0) {
+                            SS[4 * k] = ((u64)sw[1] << 32) | sw[0];
+                            SS[4 * k + 1] = ((u64)sw[3] << 32) | sw[2];
+                            SS[4 * k + 2] = ((u64)sw[5] << 32) | sw[4];
+                            SS[4 * k + 3] = ((u64)sw[7] << 32) | sw[6];
+                        }
+                    }
+                    __syncthreads();
+                    for (u32 k = w; k < n1; k += NW) {
+                        const u64* Sk = SS + 4 * k;
+                        const u32 nl = compact_bits(Sk, 0, 4, LW);
+                        for (u32 f = lane; f < nl; f += 32) {
+                            const u32 l = LW[f];
+                            const u64* Sl = SS + 4 * l;
+#pragma unroll
+                            for (u32 q = 0; q < 4; ++q)
+                                if (q >= (l >> 6)) acc += (u64)__popcll(Sk[q] & Sl[q]);
+                        }
+                        __syncwarp();
+                    }
+                    __syncthreads();
                 }
             }
         }

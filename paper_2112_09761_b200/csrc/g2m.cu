@@ -2028,6 +2028,11 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     const bool one_stream = want_streams == 1;
     const int nstreams = std::min(want_streams, (int)DevState::kSide);
     int nside = 0;
+    if constexpr (K == 5) {
+        // G2M_CL5_BIG=0: rows with 128 < |R_i| <= 256 stay on the per-warp path
+        const u32 big = getenv("G2M_CL5_BIG") ? (u32)atoi(getenv("G2M_CL5_BIG")) : 1u;
+        G2M_CUDA(cudaMemcpyToSymbolAsync(g2m_clique::g_cl5_big, &big, 4, 0, cudaMemcpyHostToDevice, st->stream));
+    }
     G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
     auto timed = [&](auto&& fn) -> int {
         if (!serial && one_stream) {

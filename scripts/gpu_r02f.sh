@@ -12,3 +12,5 @@ done
 # 4-cycle tier breakdown at RMAT-25 and RMAT-27 (G2M_DEBUG per-tier times)
 AB_REPS=1 timeout 900 python scripts/ab_env.py 25 c4 "X=0" debug > gpurun_out/${T}_c425_tiers.txt 2>&1; echo c425 rc=$?; grep -E "cycle4|c4 " gpurun_out/${T}_c425_tiers.txt | head -20
 AB_REPS=1 timeout 1200 python scripts/ab_env.py 27 c4 "X=0" debug > gpurun_out/${T}_c427_tiers.txt 2>&1; echo c427 rc=$?; grep -E "cycle4|c4 " gpurun_out/${T}_c427_tiers.txt | head -20
+timeout 600 python -m pytest tests/test_gpu_round2.py -q -k "cl5_deferred" > gpurun_out/${T}_pytest_cl5.log 2>&1; echo cl5 test rc=$?; tail -2 gpurun_out/${T}_pytest_cl5.log
+AB_REPS=3 timeout 900 python scripts/ab_env.py 22 cl5 "G2M_CL5_BIG=0|G2M_CL5_BIG=1" debug > gpurun_out/${T}_cl5_ab.txt 2>&1; echo cl5 ab rc=$?; grep -E "cl5 \[|launch" gpurun_out/${T}_cl5_ab.txt

@@ -283,3 +283,18 @@ def test_device_hub_partition_equals_reference_restatement(n):
         assert np.array_equal(part.owned_local, owned)
         assert np.array_equal(part.local_to_global, verts)
         assert np.array_equal(part.subgraph.labels, g.labels[verts])
+
+
+def test_cl5_deferred_big_rows(monkeypatch):
+    # k = 5 rows with 128 < |R_i| <= 256 go to the CTA-wide compressed phase;
+    # a dense RMAT has them (oriented hubs with d+ > 256)
+    g = GR.from_edges_device(G.rmat_edges(16, 48, 2), num_vertices=1 << 16)
+    og = pm.orient(g)
+    assert og.max_degree > 256
+    f = PL.as_forest(make_plan(P.generate_clique(5), g, oriented=True))
+    tasks = EX._default_tasks(og, f)
+    want = EX.execute(og, f, tasks, lgs=False)[0]
+    for big in ("1", "0"):
+        monkeypatch.setenv("G2M_CL5_BIG", big)
+        og2 = pm.orient(g)
+        assert EX.execute(og2, f, EX._default_tasks(og2, f))[0] == want, big
