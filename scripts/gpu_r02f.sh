@@ -1,16 +1,15 @@
-# round 2: compute-sanitizer (memcheck, racecheck, synccheck) on the small workload, the
-# multi-GPU split simulations (estimator chunk sizes vs one-by-one), then the ncu sweep
+# round 2: k=5 big-row phase (test + A/B), multi-GPU split simulations, 4-cycle tier
+# breakdown at RMAT-25/27, then compute-sanitizer (memcheck, racecheck, synccheck)
 mkdir -p gpurun_out
 T=${1:-r02f}
-for tool in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_workload.py 10 > gpurun_out/${T}_sanitize_${tool}.log 2>&1; echo $tool rc=$?; grep -E "ERROR SUMMARY|MISMATCHES|Error" gpurun_out/${T}_sanitize_${tool}.log | head -5
-done
+timeout 600 python -m pytest tests/test_gpu_round2.py -q -k "cl5_deferred" > gpurun_out/${T}_pytest_cl5.log 2>&1; echo cl5 test rc=$?; tail -2 gpurun_out/${T}_pytest_cl5.log
+AB_REPS=3 timeout 900 python scripts/ab_env.py 22 cl5 "G2M_CL5_BIG=0|G2M_CL5_BIG=1" debug > gpurun_out/${T}_cl5_ab.txt 2>&1; echo cl5 ab rc=$?; grep -E "cl5 \[|launch" gpurun_out/${T}_cl5_ab.txt
 for w in cl4 tc c4; do
   G2M_SIM_SPLITS=est:1,est:16,est:64,est:256,rr:1 timeout 1200 python bench.py --workload $w --steps 1 --warmup 1 --simulate-parts 8 --no-cpu-baseline --no-e2e --no-parity --no-roofline > gpurun_out/${T}_sim_${w}.json 2> gpurun_out/${T}_sim_${w}.err
   echo $w rc=$?; grep "simulated split" gpurun_out/${T}_sim_${w}.err
 done
-# 4-cycle tier breakdown at RMAT-25 and RMAT-27 (G2M_DEBUG per-tier times)
 AB_REPS=1 timeout 900 python scripts/ab_env.py 25 c4 "X=0" debug > gpurun_out/${T}_c425_tiers.txt 2>&1; echo c425 rc=$?; grep -E "cycle4|c4 " gpurun_out/${T}_c425_tiers.txt | head -20
 AB_REPS=1 timeout 1200 python scripts/ab_env.py 27 c4 "X=0" debug > gpurun_out/${T}_c427_tiers.txt 2>&1; echo c427 rc=$?; grep -E "cycle4|c4 " gpurun_out/${T}_c427_tiers.txt | head -20
-timeout 600 python -m pytest tests/test_gpu_round2.py -q -k "cl5_deferred" > gpurun_out/${T}_pytest_cl5.log 2>&1; echo cl5 test rc=$?; tail -2 gpurun_out/${T}_pytest_cl5.log
-AB_REPS=3 timeout 900 python scripts/ab_env.py 22 cl5 "G2M_CL5_BIG=0|G2M_CL5_BIG=1" debug > gpurun_out/${T}_cl5_ab.txt 2>&1; echo cl5 ab rc=$?; grep -E "cl5 \[|launch" gpurun_out/${T}_cl5_ab.txt
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_workload.py 10 > gpurun_out/${T}_sanitize_${tool}.log 2>&1; echo $tool rc=$?; grep -E "ERROR SUMMARY|MISMATCHES|Error" gpurun_out/${T}_sanitize_${tool}.log | head -5
+done
