@@ -256,6 +256,30 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
 }
 
 // ---------------------------------------------------------------------------
+// Hub core: the DAG restricted to the top T ranks (rank space: every out-
+// neighbour of a core vertex is in the core) as a packed upper-triangular bit
+// matrix, row alpha = a - lo holding bits beta - alpha - 1 for the core ranks
+// beta > alpha, each row padded to u32 words. T = 2^15 is 64 MB: L2-resident.
+// An edge test a -> b with a in the core is one bit read instead of a
+// binary search of N+(a) (a chain of dependent L2 reads).
+// ---------------------------------------------------------------------------
+struct HubCore {
+    const u32* bits;    // nullptr: no core
+    u32 lo, T;
+    // words of rows 0..alpha-1: S(T-1) - S(T-1-alpha), S(N) = sum_{m<=N} ceil(m/32)
+    __device__ __forceinline__ static u64 S(u64 N) {
+        const u64 q = N >> 5, r = N & 31u;
+        return 16ull * q * (q + 1) + r * (q + 1);
+    }
+    __device__ __forceinline__ bool has(u32 a, u32 b) const {
+        const u32 al = a - lo, be = b - lo;
+        const u32 bit = be - al - 1u;
+        const u64 w = S((u64)T - 1) - S((u64)T - 1 - al) + (bit >> 5);
+        return (__ldg(bits + w) >> (bit & 31u)) & 1u;
+    }
+};
+
+// ---------------------------------------------------------------------------
 // pair tier: d <= 64, one warp per source; the local edges a -> b (a, b in A)
 // are found by testing every pair of A directly, b in N+(a) by binary search
 // -- d(d-1)/2 lane-parallel tests instead of streaming the out-lists of A,
@@ -264,7 +288,7 @@ k_clique_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u3
 template <int K, int WPB, int MAXD = 64>
 __global__ void __launch_bounds__(WPB * 32)
 k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-               u64 nverts, u64* next, u64 grab, u64* count) {
+               u64 nverts, u64* next, u64 grab, u64* count, HubCore core = HubCore{nullptr, 0, 0}) {
     static_assert(K == 3 || MAXD <= 64 || (K == 4 && MAXD <= 128), "row width");
     constexpr int RW = MAXD > 64 ? 2 : 1;      // u64 words per local row
     __shared__ u32 sA[WPB][MAXD];
@@ -298,8 +322,14 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
                 while ((i + 1) * (2 * d - i - 2) / 2 <= p) ++i;
                 const u32 j = i + 1 + (p - i * (2 * d - i - 1) / 2);
                 const u32 a = A[i];
-                const u64 ao = __ldg(off + a);
-                if (g2m_has_g(nbr + ao, (u32)(__ldg(off + a + 1) - ao), A[j])) {
+                bool e;
+                if (core.bits && a >= core.lo) {
+                    e = core.has(a, A[j]);
+                } else {
+                    const u64 ao = __ldg(off + a);
+                    e = g2m_has_g(nbr + ao, (u32)(__ldg(off + a + 1) - ao), A[j]);
+                }
+                if (e) {
                     if constexpr (K == 3) acc += 1;
                     else atomicOr((u32*)(R + i * RW) + (j >> 5), 1u << (j & 31u));
                 }
@@ -1088,6 +1118,21 @@ __global__ void k_sum_choose2(const u32* t, u64 n, u64* count) {
     }
     acc = g2m_wsum(acc);
     if ((threadIdx.x & 31) == 0 && acc) g2m_add128(count, acc, 0);
+}
+
+// Hub-core bits (HubCore): one warp per core vertex a, a bit per out-neighbour.
+__global__ void k_core_build(const u64* off, const u32* nbr, u64 nv, u32 lo, u32 T, u32* bits) {
+    const u32 lane = g2m_lane();
+    for (u64 al = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; al < T;
+         al += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u64 a = lo + al;
+        const u64 b0 = off[a], b1 = off[a + 1];
+        const u64 base = HubCore::S((u64)T - 1) - HubCore::S((u64)T - 1 - al);
+        for (u64 s = b0 + lane; s < b1; s += 32) {
+            const u32 bit = nbr[s] - (u32)a - 1u;
+            atomicOr(bits + base + (bit >> 5), 1u << (bit & 31u));
+        }
+    }
 }
 
 }  // namespace g2m_clique

@@ -247,6 +247,9 @@ struct g2m_graph {
     // id of the first owned vertex (owned vertices are consecutive)
     DevBuf l2g;
     uint64_t part_first = 0, part_owned = 0;
+    // oriented graphs: the hub core of the rank-space DAG (g2m_clique::HubCore)
+    DevBuf core_bits;
+    uint32_t core_lo = 0, core_T = 0;
 };
 
 // out[0] = max degree, out[1] = Σ degree² (the BFS frontier bound, executor.choose_search)
@@ -1290,6 +1293,34 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     return G2M_OK;
 }
 
+// The hub core of an oriented graph's rank-space DAG: the top T = 2^G2M_PAIR_CORE
+// ranks (default 15; 0 = off) as a packed bit matrix (built once, cached).
+static g2m_clique::HubCore ensure_core(const g2m_graph* cg, DevState* st) {
+    g2m_graph* g = const_cast<g2m_graph*>(cg);
+    std::lock_guard<std::mutex> lk(g->mu);
+    g2m_clique::HubCore hc{nullptr, 0, 0};
+    const char* e = getenv("G2M_PAIR_CORE");
+    const int lg = e ? atoi(e) : 15;
+    if (lg <= 0 || !g->oriented || !g->has_rank || g->rk_down || g->nv < 2) return hc;
+    const u64 T = std::min<u64>((u64)1 << std::min(lg, 20), g->nv);
+    if (g->core_T != T) {
+        const u64 q = (T - 1) >> 5, r = (T - 1) & 31u;
+        const u64 words = 16ull * q * (q + 1) + r * (q + 1) + 1;
+        if (g->core_bits.ensure(words * 4) != G2M_OK) { cudaGetLastError(); return hc; }
+        cudaMemsetAsync(g->core_bits.p, 0, words * 4, st->stream);
+        g->core_lo = (uint32_t)(g->nv - T);
+        ++st->launches;
+        g2m_clique::k_core_build<<<grid_for(st, T * 32, 256), 256, 0, st->stream>>>(
+            g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), g->nv, g->core_lo, (u32)T, g->core_bits.as<u32>());
+        if (cudaGetLastError() != cudaSuccess) return hc;
+        g->core_T = (uint32_t)T;
+    }
+    hc.bits = g->core_bits.as<u32>();
+    hc.lo = g->core_lo;
+    hc.T = g->core_T;
+    return hc;
+}
+
 extern "C" int g2m_graph_reduced_tasks(const g2m_graph* g, uint64_t* out) {
     if (!g || !out) return fail(G2M_EUSAGE, "null argument");
     DevState* st;
@@ -2004,7 +2035,7 @@ static u64 pair_maxd_tc(u64 nv) {
 template <int K, bool SUP = false>
 static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const u32* lists, u64 stride,
                              const uint64_t* sizes, const uint32_t* spans, u64* ctr, double* kms,
-                             u32* tsup = nullptr) {
+                             u32* tsup = nullptr, g2m_clique::HubCore core = g2m_clique::HubCore{nullptr, 0, 0}) {
     using namespace g2m_clique;
     u64* count = ctr;        // (lo, hi)
     u64* next = ctr + 2;     // one work counter per launch
@@ -2177,13 +2208,13 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
             ++st->launches;
             if constexpr (K == 3)
                 k_clique_pairs<K, WPB, 256><<<st->sms * 8, WPB * 32, 0, ss>>>(
-                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count, core);
             else if constexpr (K == 4)
                 k_clique_pairs<K, WPB, 128><<<st->sms * 8, WPB * 32, 0, ss>>>(
-                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count, core);
             else
                 k_clique_pairs<K, WPB><<<st->sms * 8, WPB * 32, 0, ss>>>(
-                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count);
+                    off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count, core);
         }));
         ++slot;
     }
@@ -2312,6 +2343,7 @@ static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
     const u64* wpre = nullptr;
     u64 wchunk = 0;
     G2M_TRY(source_weights(g, st, part, 0, k, &wpre, &wchunk));
+    const g2m_clique::HubCore core = ensure_core(g, st);
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
     // counters: ctr[8..9] count (lo, hi), ctr[10..] one work counter per launch
     G2M_TRY(st->counters.ensure(32 * 8));
@@ -2350,9 +2382,9 @@ static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
         u64* blk = ctr + 8;
         int rc;
         switch (k) {
-        case 3: rc = clique_launch_all<3>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms); break;
-        case 4: rc = clique_launch_all<4>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms); break;
-        default: rc = clique_launch_all<5>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms); break;
+        case 3: rc = clique_launch_all<3>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms, nullptr, core); break;
+        case 4: rc = clique_launch_all<4>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms, nullptr, core); break;
+        default: rc = clique_launch_all<5>(off, nbr, st, lists, stride, sizes, spans, blk, &S->kernel_ms, nullptr, core); break;
         }
         if (rc != G2M_OK) return rc;
     }
