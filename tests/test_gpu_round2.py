@@ -298,3 +298,15 @@ def test_cl5_deferred_big_rows(monkeypatch):
         monkeypatch.setenv("G2M_CL5_BIG", big)
         og2 = pm.orient(g)
         assert EX.execute(og2, f, EX._default_tasks(og2, f))[0] == want, big
+
+
+@pytest.mark.parametrize("core", ["0", "3", "9", "15"])
+def test_hub_core_pair_tests(monkeypatch, core):
+    # pair-tier edge tests through the hub-core bit matrix (top 2^core ranks)
+    g = GR.from_edges(G.rmat_edges(14, 16, 9), num_vertices=1 << 14)
+    monkeypatch.setenv("G2M_PAIR_CORE", core)
+    og = pm.orient(g)
+    for k in (3, 4, 5):
+        f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
+        tasks = EX._default_tasks(og, f)
+        assert EX.execute(og, f, tasks)[0] == EX.execute(og, f, tasks, lgs=False)[0], (core, k)
