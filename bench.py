@@ -601,7 +601,7 @@ def main():
         prof = binding_from_profiles(args.workload, graph_key) if world == 1 else None
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm if achieved else None,
-                "traffic": prof.get("dram_bytes_per_step") if prof else None,
+                "traffic": prof.get("dram_bytes_per_step") if prof and not prof.get("counters_missing") else None,
                 "peak_source": "of measured: MEASURED_PEAKS.json hbm_gbs (copy)" if pk.get("hbm_gbs")
                 else "of fallback 6650 (B200_PROFILING.md)",
                 "algorithmic_bytes_per_step": ob,
@@ -615,7 +615,7 @@ def main():
                 "kernel_share": kms / ms if ms else None,
                 "binding": prof.get("binding") if prof else None,
                 "physical_dram_frac": (prof["dram_bytes_per_step"] / (kms / 1000.0) / 1e9 / hbm)
-                if prof and prof.get("dram_bytes_per_step") else None,
+                if prof and prof.get("dram_bytes_per_step") and not prof.get("counters_missing") else None,
                 "ncu_source": prof.get("source") if prof else None,
                 "reference_equivalent_bytes_per_step": balg,
                 "reference_equivalent_gbs": balg / (kms / 1000.0) / 1e9 if balg else None,

@@ -11,6 +11,3 @@ for w in cl4 tc c4; do
 done
 AB_REPS=1 timeout 900 python scripts/ab_env.py 25 c4 "X=0" debug > gpurun_out/${T}_c425_tiers.txt 2>&1; echo c425 rc=$?; grep -E "cycle4|c4 " gpurun_out/${T}_c425_tiers.txt | head -20
 AB_REPS=1 timeout 1200 python scripts/ab_env.py 27 c4 "X=0" debug > gpurun_out/${T}_c427_tiers.txt 2>&1; echo c427 rc=$?; grep -E "cycle4|c4 " gpurun_out/${T}_c427_tiers.txt | head -20
-for tool in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_workload.py 10 > gpurun_out/${T}_sanitize_${tool}.log 2>&1; echo $tool rc=$?; grep -E "ERROR SUMMARY|MISMATCHES|Error" gpurun_out/${T}_sanitize_${tool}.log | head -5
-done

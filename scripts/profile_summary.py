@@ -18,7 +18,13 @@ import sys
 from pathlib import Path
 
 rep, key, out = sys.argv[1], sys.argv[2], Path(sys.argv[3])
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv.gz"):          # the raw page saved on the GPU box
+    import gzip
+    raw = gzip.open(rep, "rt").read()
+elif rep.endswith(".csv"):
+    raw = Path(rep).read_text()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 H, U = rows[0], rows[1]
 
@@ -90,13 +96,21 @@ for r in rows[2:]:
 
 dram_total = sum(k["dram"] for k in kern if k["dram"] == k["dram"])
 ms_total = sum(k["ms"] for k in kern if k["ms"] == k["ms"])
-# the dominant kernel (name) = most summed time over its launches
+# the dominant kernel (name) = most summed time over its launches; ncu reports
+# -nan for the counters of some long launches (seconds-long kernels whose
+# replays it could not complete): the binding then comes from the longest
+# kernel that has counters, and the summary says so
 by = {}
 for k in kern:
     by.setdefault(k["name"], []).append(k)
 dom_name = max(by, key=lambda n: sum(x["ms"] for x in by[n]))
-dk = by[dom_name]
-w = sum(x["ms"] for x in dk) or 1.0
+with_ctr = {n: v for n, v in by.items() if any(x["issue"] == x["issue"] for x in v)}
+missing = [n for n in by if n not in with_ctr]
+bind_name = dom_name if dom_name in with_ctr else (max(with_ctr, key=lambda n: sum(x["ms"] for x in with_ctr[n]))
+                                                   if with_ctr else dom_name)
+dk = by[bind_name]
+w = sum(x["ms"] for x in by[dom_name]) or 1.0
+wb = sum(x["ms"] for x in dk) or 1.0
 
 
 def wavg(f):
@@ -107,15 +121,20 @@ def wavg(f):
 res = {"dram": wavg("dram_pct") / 100, "l2": wavg("l2_pct") / 100, "issue": wavg("issue") / 100}
 bind = max(res, key=res.get)
 lines += ["",
-          f"DRAM bytes over the captured kernels: {dram_total / 1e9:.3f} GB in {ms_total:.2f} ms (serialised, cold).",
-          f"Dominant kernel: `{dom_name}` ({w:.2f} ms, {w / (ms_total or 1) * 100:.0f}% of the captured time); "
-          f"time-weighted DRAM {res['dram'] * 100:.1f}%, L2 {res['l2'] * 100:.1f}%, issue {res['issue'] * 100:.1f}% "
-          f"of peak -> binding resource: **{bind}**."]
+          f"DRAM bytes over the captured kernels with counters: {dram_total / 1e9:.3f} GB; "
+          f"captured time {ms_total:.2f} ms (serialised, cold).",
+          f"Dominant kernel: `{dom_name}` ({w:.2f} ms, {w / (ms_total or 1) * 100:.0f}% of the captured time)."]
+if missing:
+    lines.append(f"ncu returned no counters (-nan) for: {', '.join('`%s`' % n for n in missing)} -- "
+                 f"their stall-reason samples above are valid; the binding below is from `{bind_name}`.")
+lines.append(f"Binding (`{bind_name}`, {wb:.2f} ms): time-weighted DRAM {res['dram'] * 100:.1f}%, "
+             f"L2 {res['l2'] * 100:.1f}%, issue {res['issue'] * 100:.1f}% of peak -> **{bind}**.")
 out.write_text("\n".join(lines) + "\n")
 sj = Path(sys.argv[4] if len(sys.argv) > 4 else "profiles/ncu_summary.json")
 d = json.loads(sj.read_text()) if sj.exists() else {}
 d[key] = {"dram_bytes_per_step": int(dram_total), "captured_ms": ms_total,
-          "binding": {"kernel": dom_name, "resource": bind, "frac": res[bind],
+          "dominant_kernel": dom_name, "counters_missing": missing,
+          "binding": {"kernel": bind_name, "resource": bind, "frac": res[bind],
                       "dram_frac": res["dram"], "l2_frac": res["l2"], "issue_frac": res["issue"],
                       "warp_exec_eff": wavg("eff") / 100},
           "source": f"{out} (ncu --set full, one step, sum over kernels)"}
