@@ -110,8 +110,8 @@ class RunResult:
 # ---------------------------------------------------------------------------
 
 WARPS_PER_BLOCK = 8
-SMEM_SLOT_WORDS = 4096      # per-warp shared-memory budget for slots (u32)
-STAGE_WORDS = 1024          # per-warp staging area for loop-invariant lists
+SMEM_SLOT_WORDS = int(os.environ.get("G2M_SMEM_SLOT_WORDS", 4096))  # per-warp shared budget for slots (u32)
+STAGE_WORDS = int(os.environ.get("G2M_STAGE_WORDS", 1024))          # per-warp staging of loop-invariant lists
 
 
 class CompiledPlan:
