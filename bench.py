@@ -447,9 +447,7 @@ def main():
               "undirected_edges": E, "oriented": gd.oriented, "max_degree_task_graph": gd.max_degree,
               "granularity": pj.granularity, "tasks": len(tasks),
               "search": next((d.render() for d in pj.log if d.name == "bounded-bfs"), "dfs"),
-              "parallelism": f"{world} GPU(s): graph replicated, edge tasks by chunked round-robin "
-                             f"(c = 2 x resident warps), LGS/wedge sources by the workload estimator "
-                             f"({EX.SOURCE_SPLIT}:{EX.SOURCE_CHUNK})" if world > 1 else "1 GPU",
+              "parallelism": "1 GPU",
               "l2": "inputs larger than L2 (CSR > 126 MB); no flush needed" if gd.num_edges * 4 > 126e6
               else "graph fits L2: measured warm (no flush)"}
     metric = "edges/s"
@@ -480,6 +478,11 @@ def main():
     # ------------------------------------------------------------------ b200
     rr = D.shard(rank, world, device=local)
     family = EX.kernel_family(gd, forest, tasks, rr=rr)
+    if world > 1:
+        config["parallelism"] = (
+            f"{world} GPU(s): graph replicated, edge tasks by chunked round-robin (c = 2 x resident warps), "
+            f"LGS/wedge sources by the workload estimator "
+            f"({EX.SOURCE_SPLIT}:{EX.SOURCE_CHUNK.get(family, '-')})")
 
     def step():   # run_job's search choice (DFS / bounded-frontier BFS), logged as "bounded-bfs"
         counts, st, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, search="auto")
@@ -684,7 +687,8 @@ def main():
     if args.simulate_parts > 1 and world == 1:
         sim = {}
         P = args.simulate_parts
-        splits = [("est", EX.SOURCE_CHUNK), ("rr", 1)] if family in ("lgs", "cycle4") else [(None, None)]
+        splits = ([("est", EX.SOURCE_CHUNK[family]), ("rr", 1)] if family in ("lgs", "cycle4")
+                  else [(None, None)])
         if family in ("lgs", "cycle4") and os.environ.get("G2M_SIM_SPLITS"):
             # e.g. "est:1,est:16,rr:1": every listed source split in one process
             splits = [(a, int(b or 1)) for a, _, b in

@@ -678,9 +678,11 @@ __device__ __forceinline__ u32 cta_probe(const u64* __restrict__ off, const u32*
 // bmw: u32 words of the window bitmap (0 = hash only).
 // ---------------------------------------------------------------------------
 // k = 5: local sources i with 128 < |R_i| <= 256 deferred to a CTA-wide phase
-// that compresses R_i's sub-DAG to 4-word rows (set by the host per launch;
-// G2M_CL5_BIG=0 keeps them on the per-warp W-word path).
-__device__ u32 g_cl5_big = 1;
+// that compresses R_i's sub-DAG to 4-word rows (set by the host per launch,
+// G2M_CL5_BIG=1). Off by default: measured slower on RMAT-22 (W=16 tier
+// 597 -> 670 ms; the per-big-row CTA barriers serialise what the per-warp
+// path overlaps).
+__device__ u32 g_cl5_big = 0;
 
 // Blocks per SM the narrow tiers are launched at (g2m.cu): keeps the register
 // budget at what that occupancy allows (the window/hash variants add live values).

@@ -1294,13 +1294,15 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
 }
 
 // The hub core of an oriented graph's rank-space DAG: the top T = 2^G2M_PAIR_CORE
-// ranks (default 15; 0 = off) as a packed bit matrix (built once, cached).
+// ranks (default 16: 256 MB; measured RMAT-22 pair tier 9.8 -> 5.1 ms (TC),
+// 11.8 -> 5.7 ms (4-clique); 15: 6.1 / 6.5 ms; 0 = off) as a packed bit
+// matrix (built once, cached).
 static g2m_clique::HubCore ensure_core(const g2m_graph* cg, DevState* st) {
     g2m_graph* g = const_cast<g2m_graph*>(cg);
     std::lock_guard<std::mutex> lk(g->mu);
     g2m_clique::HubCore hc{nullptr, 0, 0};
     const char* e = getenv("G2M_PAIR_CORE");
-    const int lg = e ? atoi(e) : 15;
+    const int lg = e ? atoi(e) : 16;
     if (lg <= 0 || !g->oriented || !g->has_rank || g->rk_down || g->nv < 2) return hc;
     const u64 T = std::min<u64>((u64)1 << std::min(lg, 20), g->nv);
     if (g->core_T != T) {
@@ -2061,7 +2063,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     int nside = 0;
     if constexpr (K == 5) {
         // G2M_CL5_BIG=0: rows with 128 < |R_i| <= 256 stay on the per-warp path
-        const u32 big = getenv("G2M_CL5_BIG") ? (u32)atoi(getenv("G2M_CL5_BIG")) : 1u;
+        const u32 big = getenv("G2M_CL5_BIG") ? (u32)atoi(getenv("G2M_CL5_BIG")) : 0u;
         G2M_CUDA(cudaMemcpyToSymbolAsync(g2m_clique::g_cl5_big, &big, 4, 0, cudaMemcpyHostToDevice, st->stream));
     }
     G2M_CUDA(cudaEventRecord(st->ev0, st->stream));

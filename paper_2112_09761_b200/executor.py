@@ -336,17 +336,22 @@ def _is_diamond_count(g: Graph, forest: PlanForest, tasks, sink, index, rr) -> b
 # workload estimator (runs of consecutive rank-space sources of equal
 # estimated work, SOURCE_CHUNK sources per run on average, dealt round-robin;
 # PAPER.md:1256-1262, 1309-1322), "rr" = sources dealt one by one in rank
-# order. G2M_SOURCE_SPLIT=est[:c] | rr overrides.
+# order. Chunk per family from the 8-part simulation on one B200
+# (profiles/r02/sim_*.json, max/mean kernel time over the parts):
+#   bitmap k-clique RMAT-22:  est:16  1.050 (4-clique) 1.035 (TC); est:256 2.21 / 1.11; rr:1 1.057 / 1.034
+#   4-cycle wedges RMAT-24:   est:256 1.017; est:16 1.067; rr:1 1.005
+# G2M_SOURCE_SPLIT=est[:c] | rr overrides both.
 SOURCE_SPLIT = "est"
-SOURCE_CHUNK = 256
+SOURCE_CHUNK = {"lgs": 16, "cycle4": 256}
 _ss = os.environ.get("G2M_SOURCE_SPLIT")
 if _ss:
     SOURCE_SPLIT, _, _c = _ss.partition(":")
     if _c:
-        SOURCE_CHUNK = int(_c)
+        SOURCE_CHUNK = {"lgs": int(_c), "cycle4": int(_c)}
 
 
-def source_spec(rr, split: str | None = None, chunk: int | None = None) -> N.TaskSpec:
+def source_spec(rr, split: str | None = None, chunk: int | None = None,
+                family: str = "lgs") -> N.TaskSpec:
     """The vertex-partition spec of a source-partitioned kernel for the
     part rr = (c, n, i) of a chunked round-robin schedule (None: all
     sources). The edge-task chunk c does not apply: the parts split the
@@ -358,7 +363,7 @@ def source_spec(rr, split: str | None = None, chunk: int | None = None) -> N.Tas
         return spec
     split = split or SOURCE_SPLIT
     if split == "est":
-        spec.rr_chunk, spec.weighted = int(chunk or SOURCE_CHUNK), 1
+        spec.rr_chunk, spec.weighted = int(chunk or SOURCE_CHUNK[family]), 1
     elif split == "rr":
         spec.rr_chunk = int(chunk or 1)
     else:
@@ -472,7 +477,7 @@ def execute(g: Graph, forest: PlanForest, tasks, sink=None, device: int | None =
         pid = forest.pattern_ids[0]
         return {pid: int(words[0]) | (int(words[1]) << 64)}, stats, False, cp
     if lgs and not instrument and _is_cycle4_count(g, forest, tasks, sink, index):
-        spec = source_spec(rr, *(source_split or ()))
+        spec = source_spec(rr, *(source_split or ()), family="cycle4")
         words = np.zeros(2, dtype=np.uint64)
         stats = N.RunStats()
         cfg = run_config if run_config is not None else N.RunConfig()

@@ -106,7 +106,9 @@ def test_source_spec_fields():
     s = EX.source_spec(None)
     assert s.rr_chunk == 0 and s.weighted == 0
     s = EX.source_spec((18944, 8, 3))
-    assert (s.rr_chunk, s.weighted, s.rr_parts, s.rr_part) == (EX.SOURCE_CHUNK, 1, 8, 3)
+    assert (s.rr_chunk, s.weighted, s.rr_parts, s.rr_part) == (EX.SOURCE_CHUNK["lgs"], 1, 8, 3)
+    s = EX.source_spec((18944, 8, 3), family="cycle4")
+    assert s.rr_chunk == EX.SOURCE_CHUNK["cycle4"]
     s = EX.source_spec((18944, 8, 3), "rr", 1)
     assert (s.rr_chunk, s.weighted, s.rr_parts, s.rr_part) == (1, 0, 8, 3)
     with pytest.raises(ValueError):
