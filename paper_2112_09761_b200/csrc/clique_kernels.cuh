@@ -693,7 +693,8 @@ __host__ __device__ constexpr int cta_min_blocks(int K, int W) {
 template <int K, int W, int NW, bool GR = false, bool SUP = false>
 __global__ void __launch_bounds__(NW * 32, cta_min_blocks(K, W))
 k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
-             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows, u32* tsup, u32 split, u32 direct_max) {
+             u64 nverts, u64* next, u64* count, u32 bmw, u64* grows, u32* tsup, u32 split, u32 direct_max,
+             HubCore core = HubCore{nullptr, 0, 0}) {
     constexpr u32 CH = 4;             // words compacted per round (<= 256 candidates)
     extern __shared__ __align__(16) u64 smem[];
     // layout: R [64W x (W+1)] u64 | T [NW x (W+1)] u64   (K > 3 only)
@@ -770,10 +771,14 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                     const u32 t = (y - a0) >> 6;
                     atomicOr(TT + (t >> 5), 1u << (t & 31u));
                 }
-                ro = __ldg(off + y);
-                rn = (u32)(__ldg(off + y + 1) - ro);
-                // out-neighbours of y are > y >= A0; drop the tail beyond A_last
-                if (rn > 64 && __ldg(nbr + ro + rn - 1) > alast) rn = g2m_lb(nbr + ro, rn, alast + 1u);
+                // hub-core rows (a suffix of A) are filled from the core bits below,
+                // not probed (no support counters through the core)
+                if (SUP || !core.bits || y < core.lo) {
+                    ro = __ldg(off + y);
+                    rn = (u32)(__ldg(off + y + 1) - ro);
+                    // out-neighbours of y are > y >= A0; drop the tail beyond A_last
+                    if (rn > 64 && __ldg(nbr + ro + rn - 1) > alast) rn = g2m_lb(nbr + ro, rn, alast + 1u);
+                }
             }
             const bool lng = rn >= kLongRow;     // probed row by row, not concatenated
             const u32 lm = __ballot_sync(G2M_FULL, lng);
@@ -861,6 +866,31 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
         else
             hits = cta_probe<K, NW, SUP>(off, nbr, A, RE, RB, LR, nlong, alast, d, tot, &s_lrow, &s_flat, R, Ws,
                                          HashProbe{HK, HV, hl, a0, alast}, S);
+        if constexpr (!SUP) {
+            // hub-core rows i (A[i] >= core.lo; every A[j], j > i, is then in the
+            // core too): R_i by one bit test per j > i, 32 j's per ballot, no probing
+            if (core.bits && alast >= core.lo) {
+                const u32 ic = g2m_lb(A, d, core.lo);
+                for (u32 i = ic + w; i < d; i += NW) {
+                    const u32 a = A[i];
+                    const u64 rowb = HubCore::S((u64)core.T - 1) - HubCore::S((u64)core.T - 1 - (a - core.lo));
+                    for (u32 j0 = (i + 1) & ~31u; j0 < d; j0 += 32) {
+                        const u32 j = j0 + lane;
+                        bool e = false;
+                        if (j > i && j < d) {
+                            const u32 bit = A[j] - a - 1u;
+                            e = (__ldg(core.bits + rowb + (bit >> 5)) >> (bit & 31u)) & 1u;
+                        }
+                        const u32 m = __ballot_sync(G2M_FULL, e);
+                        if constexpr (K == 3) {
+                            hits += lane == 0 ? (u32)__popc(m) : 0u;
+                        } else {
+                            if (lane == 0 && m) ((u32*)(R + (u64)i * Ws))[j0 >> 5] = m;
+                        }
+                    }
+                }
+            }
+        }
         if constexpr (K == 3) acc += hits;
         __syncthreads();
         if constexpr (SUP)

@@ -2108,6 +2108,9 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         *kms += ms;
         return G2M_OK;
     };
+    // G2M_CTA_CORE=0: the CTA tiers probe hub-core rows instead of reading the core bits
+    const g2m_clique::HubCore cta_core =
+        (getenv("G2M_CTA_CORE") && atoi(getenv("G2M_CTA_CORE")) == 0) ? g2m_clique::HubCore{nullptr, 0, 0} : core;
     int max_smem = 0;
     G2M_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
     int sm_smem = 0;
@@ -2151,7 +2154,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
             ++st->launches;
             kern<<<(unsigned)grid, NW * 32, smem, ss>>>(off, nbr, lists + (u64)cls * stride, sizes[cls],
                                                                  next + slot, count, bmw, grows, tsup, split,
-                                                                 direct_max);
+                                                                 direct_max, cta_core);
         }));
         ++slot;
         return G2M_OK;

@@ -300,11 +300,14 @@ def test_cl5_deferred_big_rows(monkeypatch):
         assert EX.execute(og2, f, EX._default_tasks(og2, f))[0] == want, big
 
 
-@pytest.mark.parametrize("core", ["0", "3", "9", "15"])
-def test_hub_core_pair_tests(monkeypatch, core):
-    # pair-tier edge tests through the hub-core bit matrix (top 2^core ranks)
-    g = GR.from_edges(G.rmat_edges(14, 16, 9), num_vertices=1 << 14)
+@pytest.mark.parametrize("core", ["0", "3", "9", "12", "16"])
+@pytest.mark.parametrize("cta", ["0", "1"])
+def test_hub_core_pair_tests(monkeypatch, core, cta):
+    # pair-tier edge tests and CTA-tier rows through the hub-core bit matrix
+    # (top 2^core ranks); a dense RMAT puts sources in every CTA tier
+    g = GR.from_edges(G.rmat_edges(14, 40, 9), num_vertices=1 << 14)
     monkeypatch.setenv("G2M_PAIR_CORE", core)
+    monkeypatch.setenv("G2M_CTA_CORE", cta)
     og = pm.orient(g)
     for k in (3, 4, 5):
         f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
