@@ -504,6 +504,7 @@ __global__ void k_c4_bucket(const u64* off, const u32* nbr, u64 nv, u64 rr_chunk
         if (lane == 0) {
             const int c = wsum <= 512 ? 1 : (wsum <= 8192 ? 2 : (wsum <= stage_cap ? 3 : 4));
             const u64 slot = atomicAdd(sizes + c, 1ull);
+            atomicAdd(sizes + 5 + c, wsum);     // wedge bound per tier (debug / balance)
             lists[(u64)c * stride + slot] = (u32)r;
             lows[(u64)c * stride + slot] = l1;
             if (c == 3)   // descending W (LPT order)

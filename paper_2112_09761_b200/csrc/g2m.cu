@@ -2610,26 +2610,28 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
     // lists/lows: classes 0..4 x nv u32 each; wkeys (class 3 sort keys) + sorted copy
     G2M_TRY(st->tasks_b.ensure(10 * stride * 4));
     G2M_TRY(st->matches.ensure(2 * stride * 8));
-    G2M_TRY(st->tasks_a.ensure(8 * 8));
+    G2M_TRY(st->tasks_a.ensure(16 * 8));
     u32* lists = st->tasks_b.as<u32>();
     u32* lows = lists + 5 * stride;
     u64* wkeys = st->matches.as<u64>();
     u64* wsorted = wkeys + stride;
     u64* dsizes = st->tasks_a.as<u64>();
-    G2M_CUDA(cudaMemsetAsync(dsizes, 0, 8 * 8, st->stream));
+    G2M_CUDA(cudaMemsetAsync(dsizes, 0, 16 * 8, st->stream));
     if (nv) {
         ++st->launches;
         g2m_c4::k_c4_bucket<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(
             off, nbr, nv, rr_chunk, parts, pt, wpre, wchunk, stage_cap, lists, lows, wkeys, stride, dsizes);
         G2M_CUDA(cudaGetLastError());
     }
-    uint64_t sizes[5];
-    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, 5 * 8, cudaMemcpyDeviceToHost, st->stream));
+    uint64_t sizes[10];
+    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, 10 * 8, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     if (dbg)
-        fprintf(stderr, "[g2m] cycle4: warp %llu, cta %llu, staged %llu, grid %llu sources (lo_x %u)\n",
+        fprintf(stderr, "[g2m] cycle4: warp %llu, cta %llu, staged %llu, grid %llu sources (lo_x %u); "
+                        "wedge bounds %llu %llu %llu %llu\n",
                 (unsigned long long)sizes[1], (unsigned long long)sizes[2], (unsigned long long)sizes[3],
-                (unsigned long long)sizes[4], lo_x);
+                (unsigned long long)sizes[4], lo_x, (unsigned long long)sizes[6], (unsigned long long)sizes[7],
+                (unsigned long long)sizes[8], (unsigned long long)sizes[9]);
     // the staged tier runs its largest wedge fans first
     if (sizes[3]) {
         size_t tb = 0;
