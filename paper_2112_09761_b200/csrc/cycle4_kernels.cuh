@@ -97,87 +97,6 @@ __device__ __forceinline__ void wedges32(const u64* __restrict__ off, const u32*
     __syncwarp();
 }
 
-// As wedges32, but f(x, valid) is called by all 32 lanes together (valid
-// lanes form a prefix): warp-collective callbacks (run-aggregated atomics).
-template <typename F>
-__device__ __forceinline__ void wedges32w(const u64* __restrict__ off, const u32* __restrict__ nbr,
-                                          const u32* L, u32 l1, u32 i0, u32 r1, u32 lo_x, u32* scratch, F&& f) {
-    const u32 lane = g2m_lane();
-    u32* fl_end = scratch;
-    u64* fl_base = (u64*)(scratch + 32);
-    const u32 i = i0 + lane;
-    u64 ro = 0;
-    u32 rn = 0;
-    if (i < l1) {
-        const u32 v = L[i];
-        ro = __ldg(off + v);
-        const u32 dv = (u32)(__ldg(off + v + 1) - ro);
-        const u32 s0 = (dv && __ldg(nbr + ro) < lo_x) ? g2m_lb(nbr + ro, dv, lo_x) : 0u;
-        const u32 e1 = (dv && __ldg(nbr + ro + dv - 1) < r1) ? dv : g2m_lb(nbr + ro, dv, r1);
-        rn = e1 > s0 ? e1 - s0 : 0u;
-        ro += s0;
-    }
-    const u32 incl = g2m_scan_incl(rn);
-    const u32 tot = __shfl_sync(G2M_FULL, incl, 31);
-    fl_end[lane] = incl;
-    fl_base[lane] = ro - (u64)(incl - rn);
-    __syncwarp();
-    u32 ow = 0;
-    for (u32 e0 = 0; e0 < tot; e0 += 64) {
-        const u32 ea = e0 + lane, eb = ea + 32;
-        u32 xa = 0, xb = 0;
-        if (ea < tot) {
-            while (fl_end[ow] <= ea) ++ow;
-            xa = __ldg(nbr + (fl_base[ow] + ea));
-        }
-        if (eb < tot) {
-            u32 ob = ow;
-            while (fl_end[ob] <= eb) ++ob;
-            xb = __ldg(nbr + (fl_base[ob] + eb));
-            ow = ob;
-        }
-        f(xa, ea < tot);
-        if (e0 + 32 < tot) f(xb, eb < tot);
-    }
-    __syncwarp();
-}
-
-template <typename F>
-__device__ __forceinline__ void wedge_rows_w(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* L,
-                                             u32 l1, u32 r1, u32 lo_x, u32* ctr, u32* scratch, F&& f) {
-    const u32 lane = g2m_lane();
-    for (;;) {
-        u32 i0 = 0;
-        if (lane == 0) i0 = atomicAdd(ctr, 32u);
-        i0 = __shfl_sync(G2M_FULL, i0, 0);
-        if (i0 >= l1) break;
-        wedges32w(off, nbr, L, l1, i0, r1, lo_x, scratch, f);
-    }
-}
-
-// Warp-collective bucket append: the lanes (valid ones a prefix) hold wedge
-// ends whose bucket ids come in sorted runs (a row segment is sorted), so one
-// lane per run does the shared-memory atomic for the whole run: lanes of a
-// hub's fan no longer serialise on one counter. Returns, per valid lane, its
-// slot (old counter value + position in the run); `add` = run length.
-__device__ __forceinline__ u32 run_append(u32* H, u32 b, bool v) {
-    const u32 lane = g2m_lane();
-    const u32 pb = __shfl_up_sync(G2M_FULL, b, 1);
-    const u32 vm = __ballot_sync(G2M_FULL, v);
-    const bool start = v && (lane == 0 || pb != b);
-    const u32 sm = __ballot_sync(G2M_FULL, start);
-    const u32 vend = 32u - (u32)__clz(vm);                // valid lanes: [0, vend)
-    u32 base = 0;
-    if (start) {
-        const u32 higher = lane == 31 ? 0u : (sm & ~((2u << lane) - 1u));
-        const u32 end = higher ? (u32)(__ffs(higher) - 1) : vend;
-        base = atomicAdd(H + b, end - lane);
-    }
-    const u32 rs = 31u - (u32)__clz(sm & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)));
-    base = __shfl_sync(G2M_FULL, base, v ? rs : 0u);
-    return base + lane - rs;
-}
-
 // Row batches of L in dynamic 32-row grabs from a shared (CTA) or global
 // (grid) counter; f as in wedges32.
 template <typename F>
@@ -300,8 +219,7 @@ k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* 
         for (u32 b = threadIdx.x; b < nb; b += NW * 32) H[b] = 0;
         __syncthreads();
         // 1: histogram of the wedge ends by bucket
-        wedge_rows_w(off, nbr, L, l1, r1, lo_x, &s_row, wscr,
-                     [&](u32 x, bool v) { run_append(H, v ? x >> kBucketBits : 0u, v); });
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row, wscr, [&](u32 x) { atomicAdd(H + (x >> kBucketBits), 1u); });
         __syncthreads();
         // 2: exclusive scan of the histogram (warp 0): cursors = bucket starts
         if (w == 0) {
@@ -316,9 +234,8 @@ k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* 
         }
         __syncthreads();
         // 3: scatter the wedge ends into their buckets (cursors end as bucket ends)
-        wedge_rows_w(off, nbr, L, l1, r1, lo_x, &s_row2, wscr, [&](u32 x, bool v) {
-            const u32 slot = run_append(H, v ? x >> kBucketBits : 0u, v);
-            if (v) stage[slot] = x;
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row2, wscr, [&](u32 x) {
+            stage[atomicAdd(H + (x >> kBucketBits), 1u)] = x;
         });
         __syncthreads();
         // 4: one warp per bucket counts it in its private shared counters
@@ -385,8 +302,7 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
         const u32 nb = (r1 >> kCoarseBits) + 1;
         for (u32 b = threadIdx.x; b < nb; b += NT) H[b] = 0;
         __syncthreads();
-        wedge_rows_w(off, nbr, L, l1, r1, lo_x, &s_row, wscr,
-                     [&](u32 x, bool v) { run_append(H, v ? x >> kCoarseBits : 0u, v); });
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row, wscr, [&](u32 x) { atomicAdd(H + (x >> kCoarseBits), 1u); });
         __syncthreads();
         if (w == 0) {
             u32 carry = 0;
@@ -399,9 +315,8 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
             }
         }
         __syncthreads();
-        wedge_rows_w(off, nbr, L, l1, r1, lo_x, &s_row2, wscr, [&](u32 x, bool v) {
-            const u32 slot = run_append(H, v ? x >> kCoarseBits : 0u, v);
-            if (v) stage[slot] = x;
+        wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row2, wscr, [&](u32 x) {
+            stage[atomicAdd(H + (x >> kCoarseBits), 1u)] = x;
         });
         __syncthreads();
         for (u32 b = 0; b < nb; ++b) {
