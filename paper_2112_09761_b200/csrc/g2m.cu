@@ -1294,15 +1294,15 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
 }
 
 // The hub core of an oriented graph's rank-space DAG: the top T = 2^G2M_PAIR_CORE
-// ranks (default 16: 256 MB; measured RMAT-22 pair tier 9.8 -> 5.1 ms (TC),
-// 11.8 -> 5.7 ms (4-clique); 15: 6.1 / 6.5 ms; 0 = off) as a packed bit
-// matrix (built once, cached).
+// ranks as a packed bit matrix (built once, cached). Default 17 (1 GB):
+// RMAT-22 TC 27.8 -> 17.6 ms, 4-clique 53.2 -> 34.9 ms with the CTA-tier core
+// rows (profiles/r02/core_ab.txt, ctacore_ab.txt); 0 = off.
 static g2m_clique::HubCore ensure_core(const g2m_graph* cg, DevState* st) {
     g2m_graph* g = const_cast<g2m_graph*>(cg);
     std::lock_guard<std::mutex> lk(g->mu);
     g2m_clique::HubCore hc{nullptr, 0, 0};
     const char* e = getenv("G2M_PAIR_CORE");
-    const int lg = e ? atoi(e) : 16;
+    const int lg = e ? atoi(e) : 17;
     if (lg <= 0 || !g->oriented || !g->has_rank || g->rk_down || g->nv < 2) return hc;
     const u64 T = std::min<u64>((u64)1 << std::min(lg, 20), g->nv);
     if (g->core_T != T) {
