@@ -366,6 +366,10 @@ __global__ void k_c4_base(u32 l1, const u64* __restrict__ rn, u64* rb, const u64
         rb[i] -= re[i] - rn[i];
 }
 
+// RED variant (template RED): increments without a return value (fire-and-
+// forget L2 reductions); the pair counts C(c, 2) come from k_c4_sweep, which
+// also clears the range.
+template <bool RED>
 __global__ void __launch_bounds__(512)
 k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const u64* __restrict__ rb,
           const u64* __restrict__ re, u64* ctr, u32* dense, u32 lo, u64* count) {
@@ -388,12 +392,35 @@ k_c4_grid(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rn, const
             const u64 e = e0 + k + lane;
             if (e < tot) {
                 while (__ldg(re + ow) <= e) ++ow;
-                acc += atomicAdd(dense + (__ldg(nbr + __ldg(rb + ow) + e) - lo), 1u);
+                if constexpr (RED) atomicAdd(dense + (__ldg(nbr + __ldg(rb + ow) + e) - lo), 1u);
+                else acc += atomicAdd(dense + (__ldg(nbr + __ldg(rb + ow) + e) - lo), 1u);
             }
         }
     }
     acc = g2m_wsum(acc);
     if (lane == 0 && acc) g2m_add128(count, acc, 0);
+}
+
+// Σ C(c, 2) over counters [0, n) (u32, 4 per thread as one u128 load) and clear them.
+__global__ void k_c4_sweep(u32* dense, u64 n, u64* count) {
+    u64 acc = 0;
+    const u64 n4 = n >> 2;
+    uint4* d4 = reinterpret_cast<uint4*>(dense);
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n4; i += (u64)gridDim.x * blockDim.x) {
+        const uint4 v = d4[i];
+        if (v.x | v.y | v.z | v.w) {
+            acc += (u64)v.x * (v.x - 1) / 2 + (u64)v.y * (v.y - 1) / 2 + (u64)v.z * (v.z - 1) / 2 +
+                   (u64)v.w * (v.w - 1) / 2;
+            d4[i] = make_uint4(0, 0, 0, 0);
+        }
+    }
+    for (u64 i = (n4 << 2) + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 c = dense[i];
+        acc += c * (c - (c ? 1 : 0)) / 2;
+        dense[i] = 0;
+    }
+    acc = g2m_wsum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) g2m_add128(count, acc, 0);
 }
 
 // Per v1 (rank r, this partition): l1 = |N(r) ∩ [0, r)| and the wedge bound

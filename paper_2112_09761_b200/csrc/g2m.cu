@@ -2732,6 +2732,8 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
         G2M_CUDA(cudaStreamSynchronize(st->stream));
         u32 lmax = 0;
         for (u32 l : gl) lmax = std::max(lmax, l);
+        // G2M_C4_RED=1: fire-and-forget increments + a C(c,2) sweep per range
+        const bool red = getenv("G2M_C4_RED") && atoi(getenv("G2M_C4_RED")) != 0;
         u64 range = (u64)1 << 24;
         if (const char* e = getenv("G2M_C4_RANGE")) range = std::max<u64>(1024, strtoull(e, nullptr, 10));
         range = std::min<u64>(range, stride);
@@ -2762,10 +2764,19 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
                     g2m_c4::k_c4_base<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(l1, rn, rb, re);
                     G2M_CUDA(cudaMemsetAsync(gctr, 0, 8, st->stream));
                     ++st->launches;
-                    g2m_c4::k_c4_grid<<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rn, rb, re, gctr, dense,
-                                                                           (u32)lo, count);
-                    G2M_CUDA(cudaGetLastError());
-                    G2M_CUDA(cudaMemsetAsync(dense, 0, (size_t)(hi - lo) * 4, st->stream));
+                    if (red) {
+                        g2m_c4::k_c4_grid<true><<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rn, rb, re, gctr,
+                                                                                   dense, (u32)lo, count);
+                        ++st->launches;
+                        g2m_c4::k_c4_sweep<<<grid_for(st, (hi - lo) / 4 + 1, 256), 256, 0, st->stream>>>(
+                            dense, hi - lo, count);
+                        G2M_CUDA(cudaGetLastError());
+                    } else {
+                        g2m_c4::k_c4_grid<false><<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rn, rb, re, gctr,
+                                                                                    dense, (u32)lo, count);
+                        G2M_CUDA(cudaGetLastError());
+                        G2M_CUDA(cudaMemsetAsync(dense, 0, (size_t)(hi - lo) * 4, st->stream));
+                    }
                 }
             }
             return G2M_OK;
