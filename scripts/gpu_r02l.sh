@@ -1,0 +1,7 @@
+# round 2 final sweep, part 2: config C5 on device-generated R-MAT (TC RMAT-27, 4-cycle RMAT-25/27)
+mkdir -p gpurun_out
+T=${1:-r02l}
+run() { n=$1; lim=$2; shift; shift; timeout $lim python bench.py "$@" > gpurun_out/${T}_bench_$n.json 2> gpurun_out/${T}_bench_$n.err; echo $n rc=$?; python scripts/line_summary.py gpurun_out/${T}_bench_$n.json | cut -c1-300; }
+run tc27 700 --workload tc --scale 27 --steps 3 --warmup 3
+run c425 600 --workload c4 --scale 25 --steps 2 --warmup 3
+run c427 1500 --workload c4 --scale 27 --steps 2 --warmup 3 --balg-sample 1e-5 --cpu-seconds 20
