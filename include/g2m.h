@@ -58,7 +58,7 @@
 extern "C" {
 #endif
 
-#define G2M_ABI_VERSION 5
+#define G2M_ABI_VERSION 6
 
 #define G2M_OK 0
 #define G2M_EUSAGE 1
@@ -207,6 +207,41 @@ int g2m_graph_reduced_tasks(const g2m_graph* g, uint64_t* out);
 int g2m_graph_hub_part(const g2m_graph* g, uint64_t lo, uint64_t hi, g2m_graph** out,
                        uint64_t* num_local, uint64_t* first_owned);
 int g2m_graph_local_ids(const g2m_graph* g, uint32_t* local_to_global);
+
+/* Bounded-BFS frequent subgraph mining, device side of fsm.run_bounded_bfs
+ * (replaces the level loop body of fsm.py:107-210; the canonical forms,
+ * the support / filter callbacks and the result dictionaries stay on the
+ * host). A g2m_fsm holds one BFS level: subgraphs of l edges (l <= 7) as
+ * rows (edges u64 u << 32 | v ascending, 7 per row; vertices u32 ascending,
+ * 8 per row; vertex count u8).
+ *   create   level 1: every edge u < w of a labeled graph with ok[u], ok[w]
+ *            (ok = label-frequency pruning, null = all)          fsm.py:135-146
+ *   rows     copy the rows out (subgraph_filter hook)
+ *   keep     keep the rows with keep[r] != 0
+ *   quick    group rows by quick pattern (fsm.py:40-47): *nq groups;
+ *   quick_records  12 u32 per group: k | l << 8, labels[8], position pairs
+ *            (6 bits each, (min << 3 | max), ascending) as a u64
+ *   domains  canonical id, position maps per group (host canonical forms,
+ *            fsm.py:50-80) -> unique (canon << 36 | position << 32 | vertex)
+ *            domain keys, their (canon << 4 | position) run lengths (the
+ *            domain sizes, fsm.py:158-170) and the unique parent << 32 |
+ *            child pattern pairs (fsm.py:171-175)
+ *   results  copy run keys / lengths, domain keys, parent-child pairs
+ *   extend   rows of patterns with kept[canon] grow by one adjacent edge,
+ *            new edge sets deduplicated with their parent patterns
+ *            (fsm.py:178-203) */
+typedef struct g2m_fsm g2m_fsm;
+int g2m_fsm_create(const g2m_graph* g, const uint8_t* ok_or_null, g2m_fsm** out, uint64_t* nrows);
+int g2m_fsm_destroy(g2m_fsm* f);
+int g2m_fsm_rows(const g2m_fsm* f, uint64_t* edges, uint32_t* verts, uint8_t* nverts);
+int g2m_fsm_keep(g2m_fsm* f, const uint8_t* keep, uint64_t* nrows);
+int g2m_fsm_quick(g2m_fsm* f, uint64_t* nq);
+int g2m_fsm_quick_records(const g2m_fsm* f, uint32_t* out);
+int g2m_fsm_domains(g2m_fsm* f, const uint32_t* canon, const uint32_t* nmaps, const uint32_t* map_off,
+                    const uint8_t* maps, uint64_t maps_bytes, uint64_t* ndom, uint64_t* nruns, uint64_t* npc);
+int g2m_fsm_results(const g2m_fsm* f, uint64_t* run_keys, uint64_t* run_len, uint64_t* dom_keys,
+                    uint64_t* pc_pairs);
+int g2m_fsm_extend(g2m_fsm* f, const uint8_t* kept, uint32_t ncanon, uint64_t* nrows);
 
 int g2m_kernel_compile(const char* cuda_source, const char* kernel_name,
                        const char* const* header_sources, const char* const* header_names,

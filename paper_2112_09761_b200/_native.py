@@ -17,7 +17,7 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libg2m.so"
 DEVICE_HEADER = PKG_DIR / "csrc" / "g2m_device.cuh"
 
-ABI_VERSION = 5                     # G2M_ABI_VERSION in include/g2m.h
+ABI_VERSION = 6                     # G2M_ABI_VERSION in include/g2m.h
 G2M_OK, G2M_EUSAGE, G2M_EBUDGET, G2M_ECUDA, G2M_STOPPED = 0, 1, 2, 3, 4
 TASKS_EDGE, TASKS_VERTEX = 0, 1
 SRC_IMPLICIT, SRC_PAIRS, SRC_VERTICES, SRC_INDEX = 0, 1, 2, 3
@@ -93,6 +93,16 @@ SIGNATURES = {
     "g2m_graph_rank_copy": (C.c_int, [_P, C.POINTER(_P)]),
     "g2m_graph_hub_part": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.POINTER(_P), _u64p, _u64p]),
     "g2m_graph_local_ids": (C.c_int, [_P, _u32p]),
+    "g2m_fsm_create": (C.c_int, [_P, C.POINTER(C.c_uint8), C.POINTER(_P), _u64p]),
+    "g2m_fsm_destroy": (C.c_int, [_P]),
+    "g2m_fsm_rows": (C.c_int, [_P, _u64p, _u32p, C.POINTER(C.c_uint8)]),
+    "g2m_fsm_keep": (C.c_int, [_P, C.POINTER(C.c_uint8), _u64p]),
+    "g2m_fsm_quick": (C.c_int, [_P, _u64p]),
+    "g2m_fsm_quick_records": (C.c_int, [_P, _u32p]),
+    "g2m_fsm_domains": (C.c_int, [_P, _u32p, _u32p, _u32p, C.POINTER(C.c_uint8), C.c_uint64, _u64p, _u64p,
+                                  _u64p]),
+    "g2m_fsm_results": (C.c_int, [_P, _u64p, _u64p, _u64p, _u64p]),
+    "g2m_fsm_extend": (C.c_int, [_P, C.POINTER(C.c_uint8), C.c_uint32, _u64p]),
     "g2m_kernel_work": (C.c_int, [_P, C.c_int32, _u64p]),
     "g2m_kernel_compile": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_char_p),
                                      C.POINTER(C.c_char_p), C.c_int32,

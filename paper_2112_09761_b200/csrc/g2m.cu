@@ -8,11 +8,19 @@
 #include "g2m_device.cuh"
 #include "clique_kernels.cuh"
 #include "cycle4_kernels.cuh"
+#include "fsm_kernels.cuh"
 
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 #include <cub/cub.cuh>
+#include <thrust/execution_policy.h>
+#include <thrust/scan.h>
+#include <thrust/sort.h>
+#include <thrust/unique.h>
+#include <thrust/reduce.h>
+#include <thrust/iterator/constant_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <chrono>
@@ -149,6 +157,11 @@ struct DevBuf {
     }
     template <typename T>
     T* as() const { return reinterpret_cast<T*>(p); }
+    void swap_with(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(bytes, o.bytes);
+        std::swap(s, o.s);
+    }
 };
 
 // Per-device reusable workspace (one run at a time per device).
@@ -2869,5 +2882,480 @@ extern "C" int g2m_setop_batch(int32_t device, int32_t op, uint64_t nc, const ui
     if (out_v && (op == 0 || op == 2) && na)
         G2M_CUDA(cudaMemcpyAsync(out_v, dv.p, na * 4, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return G2M_OK;
+}
+
+// ---------------------------------------------------------------------------
+// bounded-BFS frequent subgraph mining (fsm.py:107-210), device side; the
+// level loop, canonical forms and the support / filter callbacks stay in
+// Python (paper_2112_09761_b200/fsm.py)
+// ---------------------------------------------------------------------------
+
+struct g2m_fsm {
+    const g2m_graph* g = nullptr;
+    int l = 1;                       // edges per subgraph at this level
+    u64 n = 0;                       // rows
+    DevBuf ok;                       // allowed vertices (u8) or empty
+    DevBuf redges, rverts, rnv;      // rows
+    DevBuf par_off, par;             // per row: parent patterns (previous level's canonical ids)
+    DevBuf rec, qid, first;          // quick records, quick id per row, first row per quick id
+    u64 nq = 0;
+    DevBuf canon, nmaps, map_off, maps;
+    DevBuf dom;                      // unique domain keys
+    u64 ndom = 0;
+    DevBuf runs_cp, runs_n;          // (canon, position) runs of dom
+    u64 nruns = 0;
+    DevBuf pc;                       // unique parent -> child pairs
+    u64 npc = 0;
+};
+
+static auto thrust_on(DevState* st) { return thrust::cuda::par.on(st->stream); }
+
+static int fsm_alloc_rows(g2m_fsm* f, u64 n) {
+    G2M_TRY(f->redges.ensure(std::max<u64>(n, 1) * g2m_fsmk::kFsmE * 8));
+    G2M_TRY(f->rverts.ensure(std::max<u64>(n, 1) * g2m_fsmk::kFsmV * 4));
+    G2M_TRY(f->rnv.ensure(std::max<u64>(n, 1)));
+    G2M_TRY(f->par_off.ensure((n + 1) * 4));
+    return G2M_OK;
+}
+
+extern "C" int g2m_fsm_create(const g2m_graph* g, const uint8_t* ok, g2m_fsm** out, uint64_t* nrows) {
+    if (!g || !out || !nrows) return fail(G2M_EUSAGE, "null argument");
+    if (!g->labels.p) return fail(G2M_EUSAGE, "frequent subgraph mining requires a labeled graph");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    auto f = std::make_unique<g2m_fsm>();
+    f->g = g;
+    const u64 nv = g->nv;
+    const unsigned char* okp = nullptr;
+    if (ok) {
+        G2M_TRY(f->ok.ensure(std::max<u64>(nv, 1)));
+        if (nv) G2M_CUDA(cudaMemcpyAsync(f->ok.p, ok, nv, cudaMemcpyHostToDevice, st->stream));
+        okp = f->ok.as<unsigned char>();
+    }
+    DevBuf cnt, pos;
+    G2M_TRY(cnt.ensure(std::max<u64>(nv, 1) * 8));
+    G2M_TRY(pos.ensure((nv + 1) * 8));
+    if (nv) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_l1_count<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), nv,
+                                                                               okp, cnt.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), pos.as<u64>(), nv));
+    u64 n = 0;
+    G2M_CUDA(cudaMemcpyAsync(&n, pos.as<u64>() + nv, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    G2M_TRY(fsm_alloc_rows(f.get(), n));
+    G2M_CUDA(cudaMemsetAsync(f->redges.p, 0, std::max<u64>(n, 1) * g2m_fsmk::kFsmE * 8, st->stream));
+    G2M_CUDA(cudaMemsetAsync(f->rverts.p, 0, std::max<u64>(n, 1) * g2m_fsmk::kFsmV * 4, st->stream));
+    G2M_CUDA(cudaMemsetAsync(f->par_off.p, 0, (n + 1) * 4, st->stream));
+    if (nv) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_l1_fill<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), nv, okp, pos.as<u64>(), f->redges.as<u64>(), f->rverts.as<u32>(),
+            f->rnv.as<unsigned char>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    f->n = n;
+    f->l = 1;
+    *nrows = n;
+    *out = f.release();
+    return G2M_OK;
+}
+
+extern "C" int g2m_fsm_destroy(g2m_fsm* f) {
+    if (!f) return G2M_OK;
+    cudaSetDevice(f->g->dev);
+    delete f;
+    return G2M_OK;
+}
+
+extern "C" int g2m_fsm_rows(const g2m_fsm* f, uint64_t* edges, uint32_t* verts, uint8_t* nverts) {
+    if (!f) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(f->g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(f->g->dev));
+    if (f->n) {
+        if (edges) G2M_CUDA(cudaMemcpyAsync(edges, f->redges.p, f->n * g2m_fsmk::kFsmE * 8, cudaMemcpyDeviceToHost, st->stream));
+        if (verts) G2M_CUDA(cudaMemcpyAsync(verts, f->rverts.p, f->n * g2m_fsmk::kFsmV * 4, cudaMemcpyDeviceToHost, st->stream));
+        if (nverts) G2M_CUDA(cudaMemcpyAsync(nverts, f->rnv.p, f->n, cudaMemcpyDeviceToHost, st->stream));
+    }
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return G2M_OK;
+}
+
+__global__ void k_fsm_compact(const u64* redges, const u32* rverts, const unsigned char* rnv, const u32* par_off,
+                              const u32* par, const unsigned char* keep, const u64* pos, const u64* ppos, u64 n,
+                              u64* oe, u32* ov, unsigned char* onv, u32* opoff, u32* opar) {
+    for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < n; r += (u64)gridDim.x * blockDim.x) {
+        if (!keep[r]) continue;
+        const u64 p = pos[r];
+        for (int t = 0; t < g2m_fsmk::kFsmE; ++t) oe[p * g2m_fsmk::kFsmE + t] = redges[r * g2m_fsmk::kFsmE + t];
+        for (int t = 0; t < g2m_fsmk::kFsmV; ++t) ov[p * g2m_fsmk::kFsmV + t] = rverts[r * g2m_fsmk::kFsmV + t];
+        onv[p] = rnv[r];
+        u64 q = ppos[r];
+        opoff[p] = (u32)q;
+        for (u32 j = par_off[r]; j < par_off[r + 1]; ++j) opar[q++] = par[j];
+    }
+}
+
+// keep the rows with keep[r] != 0 (the subgraph_filter hook, fsm.py:140-146, 196-197)
+extern "C" int g2m_fsm_keep(g2m_fsm* f, const uint8_t* keep, uint64_t* nrows) {
+    if (!f || !keep || !nrows) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(f->g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(f->g->dev));
+    const u64 n = f->n;
+    std::vector<uint32_t> hpo(n + 1, 0);
+    if (n) G2M_CUDA(cudaMemcpyAsync(hpo.data(), f->par_off.p, (n + 1) * 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    std::vector<uint64_t> pos(n + 1, 0), ppos(n + 1, 0);
+    for (u64 r = 0; r < n; ++r) {
+        pos[r + 1] = pos[r] + (keep[r] ? 1 : 0);
+        ppos[r + 1] = ppos[r] + (keep[r] ? (hpo[r + 1] - hpo[r]) : 0);
+    }
+    const u64 m = pos[n];
+    DevBuf dk, dpos, dppos;
+    G2M_TRY(dk.ensure(std::max<u64>(n, 1)));
+    G2M_TRY(dpos.ensure((n + 1) * 8));
+    G2M_TRY(dppos.ensure((n + 1) * 8));
+    if (n) {
+        G2M_CUDA(cudaMemcpyAsync(dk.p, keep, n, cudaMemcpyHostToDevice, st->stream));
+        G2M_CUDA(cudaMemcpyAsync(dpos.p, pos.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st->stream));
+        G2M_CUDA(cudaMemcpyAsync(dppos.p, ppos.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st->stream));
+    }
+    auto o = std::make_unique<g2m_fsm>();
+    G2M_TRY(fsm_alloc_rows(o.get(), m));
+    G2M_CUDA(cudaMemsetAsync(o->redges.p, 0, std::max<u64>(m, 1) * g2m_fsmk::kFsmE * 8, st->stream));
+    G2M_TRY(o->par.ensure(std::max<u64>(ppos[n], 1) * 4));
+    if (n) {
+        ++st->launches;
+        k_fsm_compact<<<grid_for(st, n, 256), 256, 0, st->stream>>>(
+            f->redges.as<u64>(), f->rverts.as<u32>(), f->rnv.as<unsigned char>(), f->par_off.as<u32>(),
+            f->par.p ? f->par.as<u32>() : nullptr, dk.as<unsigned char>(), dpos.as<u64>(), dppos.as<u64>(), n,
+            o->redges.as<u64>(), o->rverts.as<u32>(), o->rnv.as<unsigned char>(), o->par_off.as<u32>(),
+            o->par.as<u32>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    const uint32_t tail = (uint32_t)ppos[n];
+    G2M_CUDA(cudaMemcpyAsync(o->par_off.as<u32>() + m, &tail, 4, cudaMemcpyHostToDevice, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    f->redges.swap_with(o->redges);
+    f->rverts.swap_with(o->rverts);
+    f->rnv.swap_with(o->rnv);
+    f->par_off.swap_with(o->par_off);
+    f->par.swap_with(o->par);
+    f->n = m;
+    *nrows = m;
+    return G2M_OK;
+}
+
+// group the rows by quick pattern (fsm.py:40-47); *nq distinct quick patterns
+extern "C" int g2m_fsm_quick(g2m_fsm* f, uint64_t* nq) {
+    if (!f || !nq) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(f->g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(f->g->dev));
+    const u64 n = f->n;
+    G2M_TRY(f->rec.ensure(std::max<u64>(n, 1) * g2m_fsmk::kRec * 4));
+    G2M_TRY(f->qid.ensure(std::max<u64>(n, 1) * 4));
+    DevBuf hash, rows, head, grp, err;
+    G2M_TRY(hash.ensure(std::max<u64>(n, 1) * 8));
+    G2M_TRY(rows.ensure(std::max<u64>(n, 1) * 8));
+    G2M_TRY(head.ensure(std::max<u64>(n, 1) * 8));
+    G2M_TRY(grp.ensure(std::max<u64>(n, 1) * 8));
+    G2M_TRY(err.ensure(4));
+    G2M_CUDA(cudaMemsetAsync(err.p, 0, 4, st->stream));
+    u64 groups = 0;
+    if (n) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_quick<<<grid_for(st, n, 256), 256, 0, st->stream>>>(
+            f->redges.as<u64>(), f->rverts.as<u32>(), f->rnv.as<unsigned char>(), n, f->l, f->g->labels.as<u32>(),
+            f->rec.as<u32>(), hash.as<u64>(), rows.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+        auto pol = thrust_on(st);
+        u64* hp = hash.as<u64>();
+        u64* rp = rows.as<u64>();
+        thrust::sort_by_key(pol, hp, hp + n, rp);
+        u64* hd = head.as<u64>();
+        thrust::transform(pol, thrust::counting_iterator<u64>(0), thrust::counting_iterator<u64>(n), hd,
+                          [hp] __device__(u64 i) -> u64 { return (i == 0 || hp[i] != hp[i - 1]) ? 1ull : 0ull; });
+        u64* gp = grp.as<u64>();
+        thrust::inclusive_scan(pol, hd, hd + n, gp);
+        G2M_CUDA(cudaMemcpyAsync(&groups, gp + n - 1, 8, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        G2M_TRY(f->first.ensure(std::max<u64>(groups, 1) * 8));
+        u64* fp = f->first.as<u64>();
+        u32* qp = f->qid.as<u32>();
+        thrust::for_each(pol, thrust::counting_iterator<u64>(0), thrust::counting_iterator<u64>(n),
+                         [=] __device__(u64 i) {
+                             const u64 g = gp[i] - 1;
+                             qp[rp[i]] = (u32)g;
+                             if (hd[i]) fp[g] = rp[i];
+                         });
+        ++st->launches;
+        g2m_fsmk::k_fsm_check<<<grid_for(st, n, 256), 256, 0, st->stream>>>(rp, n, f->rec.as<u32>(), fp, qp,
+                                                                            err.as<u32>());
+        G2M_CUDA(cudaGetLastError());
+    }
+    uint32_t e = 0;
+    G2M_CUDA(cudaMemcpyAsync(&e, err.p, 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    if (e) return fail(G2M_ECUDA, "quick-pattern hash collision");
+    f->nq = groups;
+    *nq = groups;
+    return G2M_OK;
+}
+
+__global__ void k_fsm_gather_rec(const u32* rec, const u64* first, u64 nq, u32* out) {
+    for (u64 q = blockIdx.x * (u64)blockDim.x + threadIdx.x; q < nq; q += (u64)gridDim.x * blockDim.x)
+        for (int w = 0; w < g2m_fsmk::kRec; ++w) out[q * g2m_fsmk::kRec + w] = rec[first[q] * g2m_fsmk::kRec + w];
+}
+
+// the quick record of every group (12 u32 each: k | l << 8, labels[8], position pairs u64)
+extern "C" int g2m_fsm_quick_records(const g2m_fsm* f, uint32_t* out) {
+    if (!f || !out) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(f->g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(f->g->dev));
+    if (!f->nq) return G2M_OK;
+    DevBuf tmp;
+    G2M_TRY(tmp.ensure(f->nq * g2m_fsmk::kRec * 4));
+    ++st->launches;
+    k_fsm_gather_rec<<<grid_for(st, f->nq, 256), 256, 0, st->stream>>>(f->rec.as<u32>(), f->first.as<u64>(), f->nq,
+                                                                         tmp.as<u32>());
+    G2M_CUDA(cudaMemcpyAsync(out, tmp.p, f->nq * g2m_fsmk::kRec * 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return G2M_OK;
+}
+
+// domains (fsm.py:158-166): canonical id and position maps per quick pattern
+// from the host; unique (canon, position, vertex) keys, their (canon, position)
+// run lengths (domain sizes), and the parent -> child pattern pairs
+extern "C" int g2m_fsm_domains(g2m_fsm* f, const uint32_t* canon, const uint32_t* nmaps, const uint32_t* map_off,
+                               const uint8_t* maps, uint64_t maps_bytes, uint64_t* ndom, uint64_t* nruns,
+                               uint64_t* npc) {
+    if (!f || !canon || !nmaps || !map_off || !ndom || !nruns || !npc) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(f->g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(f->g->dev));
+    const u64 n = f->n, nq = f->nq;
+    G2M_TRY(f->canon.ensure(std::max<u64>(nq, 1) * 4));
+    G2M_TRY(f->nmaps.ensure(std::max<u64>(nq, 1) * 4));
+    G2M_TRY(f->map_off.ensure(std::max<u64>(nq, 1) * 4));
+    G2M_TRY(f->maps.ensure(std::max<u64>(maps_bytes, 1)));
+    if (nq) {
+        G2M_CUDA(cudaMemcpyAsync(f->canon.p, canon, nq * 4, cudaMemcpyHostToDevice, st->stream));
+        G2M_CUDA(cudaMemcpyAsync(f->nmaps.p, nmaps, nq * 4, cudaMemcpyHostToDevice, st->stream));
+        G2M_CUDA(cudaMemcpyAsync(f->map_off.p, map_off, nq * 4, cudaMemcpyHostToDevice, st->stream));
+    }
+    if (maps_bytes) G2M_CUDA(cudaMemcpyAsync(f->maps.p, maps, maps_bytes, cudaMemcpyHostToDevice, st->stream));
+    DevBuf cnt, pos;
+    G2M_TRY(cnt.ensure(std::max<u64>(n, 1) * 8));
+    G2M_TRY(pos.ensure((n + 1) * 8));
+    if (n) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_dom_count<<<grid_for(st, n, 256), 256, 0, st->stream>>>(
+            f->qid.as<u32>(), f->nmaps.as<u32>(), f->rnv.as<unsigned char>(), n, cnt.as<u64>());
+    }
+    G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), pos.as<u64>(), n));
+    u64 nk = 0;
+    G2M_CUDA(cudaMemcpyAsync(&nk, pos.as<u64>() + n, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    G2M_TRY(f->dom.ensure(std::max<u64>(nk, 1) * 8));
+    auto pol = thrust_on(st);
+    u64 nu = 0;
+    if (n) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_dom_fill<<<grid_for(st, n, 256), 256, 0, st->stream>>>(
+            f->qid.as<u32>(), f->canon.as<u32>(), f->nmaps.as<u32>(), f->map_off.as<u32>(),
+            f->maps.as<unsigned char>(), f->rverts.as<u32>(), f->rnv.as<unsigned char>(), n, pos.as<u64>(),
+            f->dom.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+        u64* dp = f->dom.as<u64>();
+        thrust::sort(pol, dp, dp + nk);
+        nu = (u64)(thrust::unique(pol, dp, dp + nk) - dp);
+    }
+    // runs of (canon, position) = key >> 32
+    G2M_TRY(f->runs_cp.ensure(std::max<u64>(nu, 1) * 8));
+    G2M_TRY(f->runs_n.ensure(std::max<u64>(nu, 1) * 8));
+    u64 nr = 0;
+    if (nu) {
+        u64* dp = f->dom.as<u64>();
+        auto hi = thrust::make_transform_iterator(dp, [] __device__(u64 k) -> u64 { return k >> 32; });
+        auto ends = thrust::reduce_by_key(pol, hi, hi + nu, thrust::constant_iterator<u64>(1), f->runs_cp.as<u64>(),
+                                          f->runs_n.as<u64>());
+        nr = (u64)(ends.first - f->runs_cp.as<u64>());
+    }
+    // parent -> child pairs
+    uint32_t npar = 0;
+    if (n) G2M_CUDA(cudaMemcpyAsync(&npar, f->par_off.as<u32>() + n, 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    G2M_TRY(f->pc.ensure(std::max<u64>(npar, 1) * 8));
+    u64 np = 0;
+    if (npar) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_pc<<<grid_for(st, n, 256), 256, 0, st->stream>>>(f->qid.as<u32>(), f->canon.as<u32>(),
+                                                                          f->par_off.as<u32>(), f->par.as<u32>(), n,
+                                                                          f->pc.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+        u64* pp = f->pc.as<u64>();
+        thrust::sort(pol, pp, pp + npar);
+        np = (u64)(thrust::unique(pol, pp, pp + npar) - pp);
+    }
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    f->ndom = nu;
+    f->nruns = nr;
+    f->npc = np;
+    *ndom = nu;
+    *nruns = nr;
+    *npc = np;
+    return G2M_OK;
+}
+
+// copies: run keys (canon << 4 | position) and lengths, unique domain keys,
+// parent -> child pairs (parent << 32 | child); any pointer may be null
+extern "C" int g2m_fsm_results(const g2m_fsm* f, uint64_t* run_keys, uint64_t* run_len, uint64_t* dom_keys,
+                               uint64_t* pc_pairs) {
+    if (!f) return fail(G2M_EUSAGE, "null argument");
+    DevState* st;
+    G2M_TRY(dev_state(f->g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(f->g->dev));
+    if (run_keys && f->nruns) G2M_CUDA(cudaMemcpyAsync(run_keys, f->runs_cp.p, f->nruns * 8, cudaMemcpyDeviceToHost, st->stream));
+    if (run_len && f->nruns) G2M_CUDA(cudaMemcpyAsync(run_len, f->runs_n.p, f->nruns * 8, cudaMemcpyDeviceToHost, st->stream));
+    if (dom_keys && f->ndom) G2M_CUDA(cudaMemcpyAsync(dom_keys, f->dom.p, f->ndom * 8, cudaMemcpyDeviceToHost, st->stream));
+    if (pc_pairs && f->npc) G2M_CUDA(cudaMemcpyAsync(pc_pairs, f->pc.p, f->npc * 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    return G2M_OK;
+}
+
+// next level (fsm.py:178-203): rows of the patterns with kept[canon] != 0 grow
+// one edge; new edge sets deduplicated, each with its parent patterns
+extern "C" int g2m_fsm_extend(g2m_fsm* f, const uint8_t* kept, uint32_t ncanon, uint64_t* nrows) {
+    if (!f || !kept || !nrows) return fail(G2M_EUSAGE, "null argument");
+    if (f->l + 1 > g2m_fsmk::kFsmE) return fail(G2M_EUSAGE, "max_edges beyond 7 is not supported");
+    DevState* st;
+    G2M_TRY(dev_state(f->g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(f->g->dev));
+    const u64 n = f->n;
+    const int l = f->l;
+    DevBuf dk, cnt, pos;
+    G2M_TRY(dk.ensure(std::max<u32>(ncanon, 1)));
+    if (ncanon) G2M_CUDA(cudaMemcpyAsync(dk.p, kept, ncanon, cudaMemcpyHostToDevice, st->stream));
+    G2M_TRY(cnt.ensure(std::max<u64>(n, 1) * 8));
+    G2M_TRY(pos.ensure((n + 1) * 8));
+    const unsigned char* okp = f->ok.p ? f->ok.as<unsigned char>() : nullptr;
+    const g2m_graph* g = f->g;
+    if (n) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_extend<false><<<grid_for(st, n, 256), 256, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), okp, f->redges.as<u64>(), f->rverts.as<u32>(),
+            f->rnv.as<unsigned char>(), f->qid.as<u32>(), f->canon.as<u32>(), dk.as<unsigned char>(), n, l,
+            cnt.as<u64>(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_TRY(exclusive_scan_u64(st, cnt.as<u64>(), pos.as<u64>(), n));
+    u64 m = 0;
+    G2M_CUDA(cudaMemcpyAsync(&m, pos.as<u64>() + n, 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    DevBuf ce, cv, cnv, cpar, ch, cid, head, grp, gp, err;
+    G2M_TRY(ce.ensure(std::max<u64>(m, 1) * g2m_fsmk::kFsmE * 8));
+    G2M_TRY(cv.ensure(std::max<u64>(m, 1) * g2m_fsmk::kFsmV * 4));
+    G2M_TRY(cnv.ensure(std::max<u64>(m, 1)));
+    G2M_TRY(cpar.ensure(std::max<u64>(m, 1) * 4));
+    G2M_TRY(ch.ensure(std::max<u64>(m, 1) * 8));
+    G2M_TRY(cid.ensure(std::max<u64>(m, 1) * 8));
+    G2M_TRY(head.ensure(std::max<u64>(m, 1) * 4));
+    G2M_TRY(grp.ensure(std::max<u64>(m, 1) * 8));
+    G2M_TRY(gp.ensure(std::max<u64>(m, 1) * 8));
+    G2M_TRY(err.ensure(4));
+    G2M_CUDA(cudaMemsetAsync(err.p, 0, 4, st->stream));
+    G2M_CUDA(cudaMemsetAsync(ce.p, 0, std::max<u64>(m, 1) * g2m_fsmk::kFsmE * 8, st->stream));
+    G2M_CUDA(cudaMemsetAsync(cv.p, 0, std::max<u64>(m, 1) * g2m_fsmk::kFsmV * 4, st->stream));
+    u64 groups = 0;
+    auto pol = thrust_on(st);
+    if (m) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_extend<true><<<grid_for(st, n, 256), 256, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), okp, f->redges.as<u64>(), f->rverts.as<u32>(),
+            f->rnv.as<unsigned char>(), f->qid.as<u32>(), f->canon.as<u32>(), dk.as<unsigned char>(), n, l, nullptr,
+            pos.as<u64>(), ce.as<u64>(), cv.as<u32>(), cnv.as<unsigned char>(), cpar.as<u32>(), ch.as<u64>(),
+            cid.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+        // sort by (hash, then edge words) so equal edge sets are adjacent
+        u64* hp = ch.as<u64>();
+        u64* ip = cid.as<u64>();
+        thrust::sort_by_key(pol, hp, hp + m, ip);
+        ++st->launches;
+        g2m_fsmk::k_fsm_cand_heads<<<grid_for(st, m, 256), 256, 0, st->stream>>>(hp, ip, m, ce.as<u64>(), l,
+                                                                                 head.as<u32>(), err.as<u32>());
+        G2M_CUDA(cudaGetLastError());
+        u32* hd = head.as<u32>();
+        u64* gg = grp.as<u64>();
+        thrust::transform(pol, hd, hd + m, gg, [] __device__(u32 h) -> u64 { return (u64)h; });
+        thrust::inclusive_scan(pol, gg, gg + m, gg);
+        G2M_CUDA(cudaMemcpyAsync(&groups, gg + m - 1, 8, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        thrust::transform(pol, gg, gg + m, gg, [] __device__(u64 x) -> u64 { return x - 1; });
+    }
+    uint32_t e = 0;
+    G2M_CUDA(cudaMemcpyAsync(&e, err.p, 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    if (e) return fail(G2M_ECUDA, "subgraph edge-set hash collision");
+    auto o = std::make_unique<g2m_fsm>();
+    G2M_TRY(fsm_alloc_rows(o.get(), groups));
+    G2M_CUDA(cudaMemsetAsync(o->redges.p, 0, std::max<u64>(groups, 1) * g2m_fsmk::kFsmE * 8, st->stream));
+    G2M_CUDA(cudaMemsetAsync(o->rverts.p, 0, std::max<u64>(groups, 1) * g2m_fsmk::kFsmV * 4, st->stream));
+    u64 npairs = 0;
+    if (m) {
+        ++st->launches;
+        g2m_fsmk::k_fsm_next<<<grid_for(st, m, 256), 256, 0, st->stream>>>(
+            cid.as<u64>(), grp.as<u64>(), m, head.as<u32>(), ce.as<u64>(), cv.as<u32>(), cnv.as<unsigned char>(),
+            cpar.as<u32>(), o->redges.as<u64>(), o->rverts.as<u32>(), o->rnv.as<unsigned char>(), gp.as<u64>());
+        G2M_CUDA(cudaGetLastError());
+        u64* pp = gp.as<u64>();
+        thrust::sort(pol, pp, pp + m);
+        npairs = (u64)(thrust::unique(pol, pp, pp + m) - pp);
+    }
+    // parents per new row: counts of (group, parent) pairs per group -> offsets
+    G2M_TRY(o->par.ensure(std::max<u64>(npairs, 1) * 4));
+    DevBuf pcnt;
+    G2M_TRY(pcnt.ensure(std::max<u64>(groups, 1) * 4));
+    G2M_CUDA(cudaMemsetAsync(pcnt.p, 0, std::max<u64>(groups, 1) * 4, st->stream));
+    G2M_CUDA(cudaMemsetAsync(o->par_off.p, 0, (groups + 1) * 4, st->stream));
+    if (npairs) {
+        u64* pp = gp.as<u64>();
+        u32* pc = pcnt.as<u32>();
+        u32* pr = o->par.as<u32>();
+        thrust::for_each(pol, thrust::counting_iterator<u64>(0), thrust::counting_iterator<u64>(npairs),
+                         [=] __device__(u64 i) {
+                             atomicAdd(pc + (pp[i] >> 32), 1u);
+                             pr[i] = (u32)pp[i];
+                         });
+        thrust::exclusive_scan(pol, pc, pc + groups, o->par_off.as<u32>());
+        const uint32_t tail = (uint32_t)npairs;
+        G2M_CUDA(cudaMemcpyAsync(o->par_off.as<u32>() + groups, &tail, 4, cudaMemcpyHostToDevice, st->stream));
+    }
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    f->redges.swap_with(o->redges);
+    f->rverts.swap_with(o->rverts);
+    f->rnv.swap_with(o->rnv);
+    f->par_off.swap_with(o->par_off);
+    f->par.swap_with(o->par);
+    f->n = groups;
+    f->l = l + 1;
+    f->nq = 0;
+    *nrows = groups;
     return G2M_OK;
 }
