@@ -291,10 +291,11 @@ def kernel_operands(family: str, gd, forest, tasks, local, rank, args):
     from paper_2112_09761_b200 import executor as EX
     from paper_2112_09761_b200 import graph as GR
     if family == "lgs":
-        ob, probes, _, src = gd.device_graph(local).kernel_work(0)
-        return ob, ("bitmap LGS: per source u its offsets + N+(u), per v in N+(u) its offsets + "
-                    "N+(v) (local-graph probes): 16n + 20m + 4 sum_v d-(v)d+(v)"), \
-            {"probed_ids": probes, "sources": src}
+        ob, probes, bits, src = gd.device_graph(local).kernel_work(0)
+        return ob, ("bitmap LGS in rank space: per source u its offsets + N+(u); per member v outside "
+                    "the hub core its offsets + N+(v) (local-graph probes); per member in the core one "
+                    "4-byte core word per later member (bit tests)"), \
+            {"probed_ids": probes, "core_bit_tests": bits, "sources": src}
     if family == "cycle4":
         ob, wedges, upd, src = gd.device_graph(local).kernel_work(1)
         return ob + 8 * upd, ("wedge aggregation: per top vertex r its offsets + N<(r), per v its "

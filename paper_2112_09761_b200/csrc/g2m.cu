@@ -1404,6 +1404,42 @@ __global__ void k_work_c4(const u64* off, const u32* nbr, u64 nv, u32 lo_x, u64*
     }
 }
 
+// family 0 with the hub core (rank space): per source u, its offsets and
+// N+(u); per member v = A[i] outside the core its offsets and N+(v), per member
+// in the core one 4-byte core word per later member (the bit tests).
+// out: [0] bytes beyond the per-source 16 + 4d, [1] probed ids, [2] core bit tests.
+__global__ void k_work_clique_core(const u64* off, const u32* nbr, u64 nv, u32 core_lo, int core_on, u64* out) {
+    const u32 lane = g2m_lane();
+    u64 bytes = 0, probes = 0, bits = 0, src = 0;
+    for (u64 u = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; u < nv;
+         u += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u64 b = off[u];
+        const u32 d = (u32)(off[u + 1] - b);
+        if (d && lane == 0) ++src;
+        for (u32 i = lane; i < d; i += 32) {
+            const u32 v = __ldg(nbr + b + i);
+            if (core_on && v >= core_lo) {
+                bits += d - 1 - i;
+                bytes += 4ull * (d - 1 - i);
+            } else {
+                const u64 dv = __ldg(off + v + 1) - __ldg(off + v);
+                probes += dv;
+                bytes += 16 + 4 * dv;
+            }
+        }
+    }
+    bytes = g2m_wsum(bytes);
+    probes = g2m_wsum(probes);
+    bits = g2m_wsum(bits);
+    src = g2m_wsum(src);
+    if (lane == 0) {
+        if (bytes) atomicAdd(out, bytes);
+        if (probes) atomicAdd(out + 1, probes);
+        if (bits) atomicAdd(out + 2, bits);
+        if (src) atomicAdd(out + 3, src);
+    }
+}
+
 extern "C" int g2m_kernel_work(const g2m_graph* g, int32_t family, uint64_t* out) {
     if (!g || !out) return fail(G2M_EUSAGE, "null argument");
     if (family == 0 && !g->oriented) return fail(G2M_EUSAGE, "clique work needs an oriented graph");
@@ -1418,6 +1454,24 @@ extern "C" int g2m_kernel_work(const g2m_graph* g, int32_t family, uint64_t* out
     G2M_TRY(acc.ensure(4 * 8));
     G2M_CUDA(cudaMemsetAsync(acc.p, 0, 4 * 8, st->stream));
     uint64_t h[4] = {0, 0, 0, 0};
+    if (family == 0 && !g->rk_down) {
+        // the kernels' own work, in rank space with the hub core they use
+        G2M_TRY(ensure_rank(g, st));
+        const g2m_clique::HubCore hc = ensure_core(g, st);
+        if (nv) {
+            ++st->launches;
+            k_work_clique_core<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(
+                g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), nv, hc.lo, hc.bits ? 1 : 0, acc.as<u64>());
+            G2M_CUDA(cudaGetLastError());
+        }
+        G2M_CUDA(cudaMemcpyAsync(h, acc.p, 32, cudaMemcpyDeviceToHost, st->stream));
+        G2M_CUDA(cudaStreamSynchronize(st->stream));
+        out[0] = 16 * nv + 4 * g->slots + h[0];
+        out[1] = h[1];
+        out[2] = h[2];
+        out[3] = h[3];
+        return G2M_OK;
+    }
     if (family == 0) {
         G2M_TRY(indeg.ensure(std::max<u64>(nv, 1) * 4));
         G2M_CUDA(cudaMemsetAsync(indeg.p, 0, std::max<u64>(nv, 1) * 4, st->stream));

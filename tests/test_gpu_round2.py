@@ -117,16 +117,24 @@ def test_rank_relabel_is_idempotent_and_count_invariant():
     assert pm.k_clique(rog, 4).counts == pm.k_clique(og, 4).counts
 
 
-def test_kernel_work_counters():
+def test_kernel_work_counters(monkeypatch):
     g = GR.from_edges(G.rmat_edges(11, 16, 6), num_vertices=1 << 11)
+    monkeypatch.setenv("G2M_PAIR_CORE", "0")     # no hub core: every member's list is read
     og = orient_host(g)
-    ob, probes, _, src = og.device_graph().kernel_work(0)
+    ob, probes, bits, src = og.device_graph().kernel_work(0)
     off = np.asarray(og.row_offsets, dtype=np.int64)
     dout = np.diff(off)
     din = np.bincount(og.neighbors, minlength=og.num_vertices)
-    assert probes == int(np.dot(dout, din))
+    assert probes == int(np.dot(dout, din)) and bits == 0
     assert ob == 16 * og.num_vertices + 20 * og.num_edges + 4 * probes
     assert src == int(np.count_nonzero(dout))
+    # hub core covering the whole graph (2^17 >= |V|): one core word per later member
+    monkeypatch.setenv("G2M_PAIR_CORE", "17")
+    og2 = orient_host(g)
+    ob2, probes2, bits2, src2 = og2.device_graph().kernel_work(0)
+    pairs = int(np.sum(dout * (dout - 1) // 2))
+    assert (probes2, bits2, src2) == (0, pairs, src)
+    assert ob2 == 16 * og.num_vertices + 4 * og.num_edges + 4 * pairs
     # 4-cycle wedges in rank space: sum over r of sum over v in N(r), v < r of |N(v) & [lo, r)|
     rg = GR.rank_relabel(g)
     roff = np.asarray(rg.row_offsets, dtype=np.int64)
