@@ -304,7 +304,7 @@ def kernel_operands(family: str, gd, forest, tasks, local, rank, args):
             {"wedges": wedges, "sources": src}
     if family == "diamond":
         og = GR.orient(gd, device=local)
-        ob, probes, _, src = og.device_graph(local).kernel_work(0)
+        ob, probes, _, src = og.device_graph(local).kernel_work(2)     # support tiers: no hub core
         # + one support counter RMW per triangle edge (3 per triangle found) and
         # the final pass over the support array
         return ob + 8 * og.num_edges, ("edge triangle support on the degree-oriented DAG: the "

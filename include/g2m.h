@@ -192,7 +192,8 @@ int g2m_graph_destroy(g2m_graph* g);
 int g2m_graph_rank_copy(const g2m_graph* g, g2m_graph** out);
 /* Algorithmic work of the specialised kernels on g (bench roofline):
  * family 0 = bitmap k-clique on an oriented graph (rank space, with the hub
- * core the kernels use), 1 = 4-cycle wedges on a symmetric graph. out[0]
+ * core the kernels use; 2 = the same without the core), 1 = 4-cycle wedges on
+ * a symmetric graph. out[0]
  * operand bytes, out[1] probed ids / wedges, out[2] core bit tests (0) /
  * counter updates (1), out[3] sources with work (see g2m.cu). */
 int g2m_kernel_work(const g2m_graph* g, int32_t family, uint64_t* out);

@@ -1442,6 +1442,9 @@ __global__ void k_work_clique_core(const u64* off, const u32* nbr, u64 nv, u32 c
 
 extern "C" int g2m_kernel_work(const g2m_graph* g, int32_t family, uint64_t* out) {
     if (!g || !out) return fail(G2M_EUSAGE, "null argument");
+    // family 2 = family 0 without the hub core (the diamond support tiers probe every list)
+    const bool no_core = family == 2;
+    if (family == 2) family = 0;
     if (family == 0 && !g->oriented) return fail(G2M_EUSAGE, "clique work needs an oriented graph");
     if (family == 1 && g->oriented) return fail(G2M_EUSAGE, "4-cycle work needs a symmetric graph");
     if (family != 0 && family != 1) return fail(G2M_EUSAGE, "unknown kernel family");
@@ -1457,7 +1460,7 @@ extern "C" int g2m_kernel_work(const g2m_graph* g, int32_t family, uint64_t* out
     if (family == 0 && !g->rk_down) {
         // the kernels' own work, in rank space with the hub core they use
         G2M_TRY(ensure_rank(g, st));
-        const g2m_clique::HubCore hc = ensure_core(g, st);
+        const g2m_clique::HubCore hc = no_core ? g2m_clique::HubCore{nullptr, 0, 0} : ensure_core(g, st);
         if (nv) {
             ++st->launches;
             k_work_clique_core<<<grid_for(st, nv * 32, 256), 256, 0, st->stream>>>(
