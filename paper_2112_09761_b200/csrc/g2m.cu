@@ -2670,9 +2670,11 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
     const u32 nbmax2 = (u32)((nv >> g2m_c4::kCoarseBits) + 2 + 3) & ~3u;
     const size_t stage2_smem = g2m_c4::stage2_smem_bytes(NW2, nbmax2);
     const bool tier3 = (coarse ? stage2_smem : stage_smem) <= (size_t)max_smem;
-    // wedges per v1 staged (256 MB slab per block); RMAT-25: 16M -> 64M moves
-    // 6.3 K top vertices from the grid tier, 6.59 -> 6.48 s (c4_grid_ab.txt)
-    u64 stage_cap = tier3 ? ((u64)64 << 20) : 0;
+    // wedges per v1 staged (64 MB slab per block). 64M was measured too:
+    // RMAT-25 6.59 -> 6.48 s, but RMAT-27 58 -> 85 s (the moved top vertices
+    // have 4096 coarse buckets each; the staged tier's per-bucket barriers
+    // dominate them), so 16M.
+    u64 stage_cap = tier3 ? ((u64)16 << 20) : 0;
     if (const char* e = getenv("G2M_C4_STAGE_CAP")) stage_cap = tier3 ? strtoull(e, nullptr, 10) : 0;
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
     G2M_TRY(st->counters.ensure(32 * 8));
