@@ -267,9 +267,23 @@ k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* 
 constexpr u32 kCoarseBits = 15;
 constexpr u32 kCoarseIds = 1u << kCoarseBits;
 
+// Count-phase rounds (G2M_C4_ROUNDS): consecutive small buckets (<= kRoundEntries
+// entries in total, <= kRoundBuckets buckets) are counted together, warp-privately:
+// the round's entries are counting-sorted in shared memory by (bucket, 1024-id
+// sub-range), and each warp counts its (bucket, sub-range) groups in its own
+// 1024-counter slice of C -- a few CTA barriers per round instead of two per
+// bucket (a top vertex of RMAT-27 has up to 4096 coarse buckets, most of them
+// holding a handful of wedge ends).
+constexpr u32 kRoundEntries = 8192;
+constexpr u32 kRoundBuckets = 64;
+constexpr u32 kRoundKeys = kRoundBuckets * (kCoarseIds >> 10);   // (bucket, sub-range) groups
+
 __host__ __device__ constexpr size_t stage2_smem_bytes(int NW, u32 nbmax) {
-    return (size_t)4 * nbmax + (size_t)4 * kCoarseIds + (size_t)4 * NW * 96;
+    return (size_t)4 * nbmax + (size_t)4 * kCoarseIds + (size_t)4 * NW * 96 + (size_t)4 * kRoundEntries +
+           (size_t)4 * (kRoundKeys + 1);
 }
+
+__device__ u32 g_c4_rounds = 1;
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
@@ -283,6 +297,8 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
     const u32 lane = g2m_lane();
     const u32 w = threadIdx.x >> 5;
     u32* wscr = C + kCoarseIds + w * 96;
+    u32* RS = C + kCoarseIds + NW * 96;          // round staging [kRoundEntries]
+    u32* RK = RS + kRoundEntries;                // round group cursors [kRoundKeys + 1]
     u32* stage = stage_all + (u64)blockIdx.x * stage_cap;
     __shared__ u64 s_t;
     __shared__ u32 s_row, s_row2;
@@ -319,9 +335,56 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
             stage[atomicAdd(H + (x >> kCoarseBits), 1u)] = x;
         });
         __syncthreads();
-        for (u32 b = 0; b < nb; ++b) {
+        for (u32 b = 0; b < nb;) {
             const u32 s0 = b ? H[b - 1] : 0u, s1 = H[b];
-            if (s0 == s1) continue;
+            if (s0 == s1) { ++b; continue; }
+            if (g_c4_rounds && s1 - s0 <= kRoundEntries) {
+                // a round: buckets [b, be) with <= kRoundEntries entries in total
+                u32 be = b + 1;
+                while (be < nb && be - b < kRoundBuckets && H[be] - s0 <= kRoundEntries) ++be;
+                const u32 tot = H[be - 1] - s0;
+                const u32 nkey = (be - b) << (kCoarseBits - 10);
+                for (u32 x = threadIdx.x; x <= nkey; x += NT) RK[x] = 0;
+                __syncthreads();
+                // key = (bucket - b) * 32 + 1024-id sub-range; bucket of entry e from its id
+                for (u32 e = threadIdx.x; e < tot; e += NT) {
+                    const u32 x = stage[s0 + e];
+                    const u32 key = (((x >> kCoarseBits) - b) << (kCoarseBits - 10)) | ((x >> 10) & 31u);
+                    atomicAdd(RK + key + 1, 1u);
+                }
+                __syncthreads();
+                if (w == 0) {       // inclusive scan of RK[1..nkey] -> group starts RK[0..nkey]
+                    u32 carry = 0;
+                    for (u32 q0 = 1; q0 <= nkey; q0 += 32) {
+                        const u32 q = q0 + lane;
+                        const u32 v = q <= nkey ? RK[q] : 0u;
+                        const u32 incl = g2m_scan_incl(v);
+                        if (q <= nkey) RK[q] = carry + incl;
+                        carry += __shfl_sync(G2M_FULL, incl, 31);
+                    }
+                }
+                __syncthreads();
+                // scatter into the round staging area (group cursors start at RK[key])
+                for (u32 e = threadIdx.x; e < tot; e += NT) {
+                    const u32 x = stage[s0 + e];
+                    const u32 key = (((x >> kCoarseBits) - b) << (kCoarseBits - 10)) | ((x >> 10) & 31u);
+                    RS[atomicAdd(RK + key, 1u)] = x;
+                }
+                __syncthreads();
+                // RK[key] is now the end of group key (its start is RK[key - 1], 0 for key 0)
+                u32* Cw = C + w * 1024u;
+                for (u32 key = w; key < nkey; key += NW) {
+                    const u32 g0 = key ? RK[key - 1] : 0u, g1 = RK[key];
+                    if (g0 == g1) continue;
+                    for (u32 e = g0 + lane; e < g1; e += 32) acc += atomicAdd(Cw + (RS[e] & 1023u), 1u);
+                    __syncwarp();
+                    for (u32 e = g0 + lane; e < g1; e += 32) Cw[RS[e] & 1023u] = 0;
+                    __syncwarp();
+                }
+                __syncthreads();
+                b = be;
+                continue;
+            }
             for (u32 e = s0 + threadIdx.x; e < s1; e += NT) acc += atomicAdd(C + (stage[e] & (kCoarseIds - 1)), 1u);
             __syncthreads();
             if (s1 - s0 > kCoarseIds / 4) {
@@ -330,6 +393,7 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
                 for (u32 e = s0 + threadIdx.x; e < s1; e += NT) C[stage[e] & (kCoarseIds - 1)] = 0;
             }
             __syncthreads();
+            ++b;
         }
     }
     acc = g2m_wsum(acc);

@@ -2764,6 +2764,9 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
         }));
     }
     if (sizes[3] && coarse) {
+        // G2M_C4_ROUNDS=0: every bucket counted by the whole CTA (two barriers each)
+        const u32 rounds = getenv("G2M_C4_ROUNDS") ? (u32)atoi(getenv("G2M_C4_ROUNDS")) : 1u;
+        G2M_CUDA(cudaMemcpyToSymbolAsync(g2m_c4::g_c4_rounds, &rounds, 4, 0, cudaMemcpyHostToDevice, st->stream));
         auto kern = g2m_c4::k_c4_stage2<NW2>;
         G2M_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage2_smem));
         int occ = 0;

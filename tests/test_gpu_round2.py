@@ -323,3 +323,15 @@ def test_hub_core_pair_tests(monkeypatch, core, cta):
         f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
         tasks = EX._default_tasks(og, f)
         assert EX.execute(og, f, tasks)[0] == EX.execute(og, f, tasks, lgs=False)[0], (core, k)
+
+
+@pytest.mark.parametrize("rounds", ["0", "1"])
+def test_cycle4_coarse_staging_rounds(monkeypatch, rounds):
+    # the coarse staging tier (forced) with and without the batched count rounds
+    g = GR.from_edges(G.rmat_edges(14, 16, 8), num_vertices=1 << 14)
+    f = PL.as_forest(make_plan(cycle4(), g))
+    want = EX.execute(g, f, EX._default_tasks(g, f), lgs=False)[0]
+    monkeypatch.setenv("G2M_C4_FINE", "0")
+    monkeypatch.setenv("G2M_C4_ROUNDS", rounds)
+    g2 = GR.from_edges(G.rmat_edges(14, 16, 8), num_vertices=1 << 14)
+    assert EX.execute(g2, f, EX._default_tasks(g2, f))[0] == want
