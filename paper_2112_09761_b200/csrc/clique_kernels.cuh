@@ -315,23 +315,49 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
             __syncwarp();
             const u32 np = d * (d - 1) / 2;
             const float D = 2.f * (float)d - 1.f;
-            for (u32 p = lane; p < np; p += 32) {
-                // row i of pair p in the row-major upper triangle: closed form + fix-up
-                u32 i = (u32)((D - sqrtf(D * D - 8.f * (float)p)) * 0.5f);
-                while (i > 0 && i * (2 * d - i - 1) / 2 > p) --i;
-                while ((i + 1) * (2 * d - i - 2) / 2 <= p) ++i;
-                const u32 j = i + 1 + (p - i * (2 * d - i - 1) / 2);
-                const u32 a = A[i];
-                bool e;
-                if (core.bits && a >= core.lo) {
-                    e = core.has(a, A[j]);
-                } else {
-                    const u64 ao = __ldg(off + a);
-                    e = g2m_has_g(nbr + ao, (u32)(__ldg(off + a + 1) - ao), A[j]);
+            // PU pairs per lane per step: their core-word loads are all in flight
+            // before any is used (the core reads are the latency of this tier)
+            constexpr int PU = 4;
+            for (u32 p0 = lane; p0 < np; p0 += 32 * PU) {
+                u32 ii[PU], jj[PU], cw[PU];
+                bool vv[PU], cc[PU];
+#pragma unroll
+                for (int q = 0; q < PU; ++q) {
+                    const u32 p = p0 + 32u * q;
+                    vv[q] = p < np;
+                    cc[q] = false;
+                    ii[q] = jj[q] = cw[q] = 0u;
+                    if (vv[q]) {
+                        // row i of pair p in the row-major upper triangle: closed form + fix-up
+                        u32 i = (u32)((D - sqrtf(D * D - 8.f * (float)p)) * 0.5f);
+                        while (i > 0 && i * (2 * d - i - 1) / 2 > p) --i;
+                        while ((i + 1) * (2 * d - i - 2) / 2 <= p) ++i;
+                        ii[q] = i;
+                        jj[q] = i + 1 + (p - i * (2 * d - i - 1) / 2);
+                        const u32 a = A[i];
+                        if (core.bits && a >= core.lo) {
+                            cc[q] = true;
+                            const u32 al = a - core.lo, bit = A[jj[q]] - a - 1u;
+                            cw[q] = __ldg(core.bits + HubCore::S((u64)core.T - 1) -
+                                          HubCore::S((u64)core.T - 1 - al) + (bit >> 5)) >> (bit & 31u);
+                        }
+                    }
                 }
-                if (e) {
-                    if constexpr (K == 3) acc += 1;
-                    else atomicOr((u32*)(R + i * RW) + (j >> 5), 1u << (j & 31u));
+#pragma unroll
+                for (int q = 0; q < PU; ++q) {
+                    if (!vv[q]) continue;
+                    bool e;
+                    if (cc[q]) {
+                        e = cw[q] & 1u;
+                    } else {
+                        const u32 a = A[ii[q]];
+                        const u64 ao = __ldg(off + a);
+                        e = g2m_has_g(nbr + ao, (u32)(__ldg(off + a + 1) - ao), A[jj[q]]);
+                    }
+                    if (e) {
+                        if constexpr (K == 3) acc += 1;
+                        else atomicOr((u32*)(R + ii[q] * RW) + (jj[q] >> 5), 1u << (jj[q] & 31u));
+                    }
                 }
             }
             if constexpr (K > 3 && RW == 1) {
@@ -874,18 +900,27 @@ k_clique_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32
                 for (u32 i = ic + w; i < d; i += NW) {
                     const u32 a = A[i];
                     const u64 rowb = HubCore::S((u64)core.T - 1) - HubCore::S((u64)core.T - 1 - (a - core.lo));
-                    for (u32 j0 = (i + 1) & ~31u; j0 < d; j0 += 32) {
-                        const u32 j = j0 + lane;
-                        bool e = false;
-                        if (j > i && j < d) {
-                            const u32 bit = A[j] - a - 1u;
-                            e = (__ldg(core.bits + rowb + (bit >> 5)) >> (bit & 31u)) & 1u;
+                    // four 32-member chunks per step: four independent core-word loads in
+                    // flight per lane before the ballots (the loads are the latency)
+                    for (u32 j0 = (i + 1) & ~31u; j0 < d; j0 += 128) {
+                        u32 wv[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const u32 j = j0 + 32u * q + lane;
+                            wv[q] = 0u;
+                            if (j > i && j < d) {
+                                const u32 bit = A[j] - a - 1u;
+                                wv[q] = __ldg(core.bits + rowb + (bit >> 5)) >> (bit & 31u);
+                            }
                         }
-                        const u32 m = __ballot_sync(G2M_FULL, e);
-                        if constexpr (K == 3) {
-                            hits += lane == 0 ? (u32)__popc(m) : 0u;
-                        } else {
-                            if (lane == 0 && m) ((u32*)(R + (u64)i * Ws))[j0 >> 5] = m;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const u32 m = __ballot_sync(G2M_FULL, wv[q] & 1u);
+                            if constexpr (K == 3) {
+                                hits += lane == 0 ? (u32)__popc(m) : 0u;
+                            } else {
+                                if (lane == 0 && m) ((u32*)(R + (u64)i * Ws))[(j0 >> 5) + q] = m;
+                            }
                         }
                     }
                 }

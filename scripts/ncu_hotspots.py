@@ -49,19 +49,25 @@ if hdr_i is None:
     sys.exit(0)
 H = rows[hdr_i]
 c_samp = next(i for i, c in enumerate(H) if "Sampling" in c or "Samples" in c)
-c_src = next((i for i, c in enumerate(H) if c.strip() in ("Source", "# Source")), None)
+c_src = next((i for i, c in enumerate(H) if c.strip() in ("Source", "# Source")), None)   # the CUDA column
 c_line = next((i for i, c in enumerate(H) if c.strip() in ("#", "Line", "Line No", "# Line")), None)
 c_addr = next((i for i, c in enumerate(H) if "Address" in c), None)
 # cuda,sass view: CUDA line rows carry a line number and no address; SASS rows
 # follow their line. Aggregate SASS samples onto the preceding CUDA line.
 agg = {}
 cur = ("?", "")
-for r in rows[hdr_i + 1:]:
-    if len(r) != len(H):
+fname = "?"
+for r in rows:
+    if len(r) == 2 and r[0] == "File Path":
+        fname = r[1].split("/")[-1]
         continue
-    is_sass = c_addr is not None and r[c_addr].strip() != ""
+    if len(r) != len(H) or r[0] == H[0]:
+        continue
+    if c_addr is not None and r[c_addr].strip() == "...":
+        continue          # separator between the SASS runs of one CUDA line
+    is_sass = c_addr is not None and r[c_addr].strip().startswith("0x")
     if not is_sass:
-        cur = (r[c_line] if c_line is not None else "?", r[c_src] if c_src is not None else "")
+        cur = (f"{fname}:{r[c_line] if c_line is not None else '?'}", r[c_src] if c_src is not None else "")
         agg.setdefault(cur, 0.0)
         agg[cur] += num(r[c_samp]) if c_addr is None else 0.0
     else:
@@ -69,4 +75,4 @@ for r in rows[hdr_i + 1:]:
 tot = sum(agg.values()) or 1.0
 print(f"== {kname} (launch {skip} of [{rx}]): {int(tot)} stall samples")
 for (ln, src), v in sorted(agg.items(), key=lambda kv: -kv[1])[:top]:
-    print(f"{v / tot * 100:5.1f}%  L{ln:>5}  {src.strip()[:110]}")
+    print(f"{v / tot * 100:5.1f}%  {ln:>26}  {src.strip()[:100]}")
