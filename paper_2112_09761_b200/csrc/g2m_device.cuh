@@ -310,6 +310,7 @@ template <int NI, int NL>
 __device__ __forceinline__ u32 g2m_materialize(const u32* (&lp)[NL], u32 (&ln)[NL],
                                                const u32* labels, u32 label, u32* out) {
     const u32 lane = g2m_lane();
+    __syncwarp();          // lanes may still read out's previous contents (racecheck WAR)
     g2m_pick_stream<NI, NL>(lp, ln);
     const u32* sp = lp[0];
     const u32 sn = ln[0];
@@ -343,6 +344,7 @@ __device__ __forceinline__ u32 g2m_hits(const u32* sp, u32 cut, u32 bound, const
 // Stage a list into shared memory (coalesced copy), returns the smem view.
 __device__ __forceinline__ const u32* g2m_stage(const u32* src, u32 n, u32* dst) {
     const u32 lane = g2m_lane();
+    __syncwarp();          // previous readers of dst are done (racecheck WAR)
     for (u32 i = lane; i < n; i += 32) dst[i] = __ldg(src + i);
     __syncwarp();
     return dst;
