@@ -285,7 +285,7 @@ struct HubCore {
 // -- d(d-1)/2 lane-parallel tests instead of streaming the out-lists of A,
 // which for small sources are mostly far longer than A itself.
 // ---------------------------------------------------------------------------
-template <int K, int WPB, int MAXD = 64>
+template <int K, int WPB, int MAXD = 64, int PU = 1>
 __global__ void __launch_bounds__(WPB * 32)
 k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ verts,
                u64 nverts, u64* next, u64 grab, u64* count, HubCore core = HubCore{nullptr, 0, 0}) {
@@ -317,7 +317,6 @@ k_clique_pairs(const u64* __restrict__ off, const u32* __restrict__ nbr, const u
             const float D = 2.f * (float)d - 1.f;
             // PU pairs per lane per step: their core-word loads are all in flight
             // before any is used (the core reads are the latency of this tier)
-            constexpr int PU = 4;
             for (u32 p0 = lane; p0 < np; p0 += 32 * PU) {
                 u32 ii[PU], jj[PU], cw[PU];
                 bool vv[PU], cc[PU];

@@ -2279,16 +2279,19 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     } else if (kClasses > 8 && sizes[8]) {
         constexpr int WPB = 8;
         u64 grab = std::max<u64>(1, std::min<u64>(16, sizes[8] / ((u64)st->sms * 64 * WPB)));
+        // G2M_PAIR_PU: pair tests (core-word loads) in flight per lane per step
+        const int pu = getenv("G2M_PAIR_PU") ? atoi(getenv("G2M_PAIR_PU")) : 1;
         G2M_TRY(timed([&](cudaStream_t ss) {
             ++st->launches;
-            if constexpr (K == 3)
-                k_clique_pairs<K, WPB, 256><<<st->sms * 8, WPB * 32, 0, ss>>>(
+            constexpr int MX = K == 3 ? 256 : (K == 4 ? 128 : 64);
+            if (pu >= 4)
+                k_clique_pairs<K, WPB, MX, 4><<<st->sms * 8, WPB * 32, 0, ss>>>(
                     off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count, core);
-            else if constexpr (K == 4)
-                k_clique_pairs<K, WPB, 128><<<st->sms * 8, WPB * 32, 0, ss>>>(
+            else if (pu == 2)
+                k_clique_pairs<K, WPB, MX, 2><<<st->sms * 8, WPB * 32, 0, ss>>>(
                     off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count, core);
             else
-                k_clique_pairs<K, WPB><<<st->sms * 8, WPB * 32, 0, ss>>>(
+                k_clique_pairs<K, WPB, MX, 1><<<st->sms * 8, WPB * 32, 0, ss>>>(
                     off, nbr, lists + 8 * stride, sizes[8], next + slot, grab, count, core);
         }));
         ++slot;
