@@ -540,7 +540,7 @@ def main():
             for gg in {id(g): g, id(gd): gd}.values():
                 gg.drop_device_copies()
         e2e_s = []
-        nw = max(1, args.warmup // 2)
+        nw = max(2, args.warmup)       # the memory pool settles over the first fresh graphs
         for i in range(nw + args.steps):
             if dist is not None:
                 dist.barrier()
