@@ -13,7 +13,14 @@ cap() {  # tag env regex skip count bench-args
   done
   ls -la gpurun_out/${T}_${tag}*
 }
-cap cl4 "X=0" "k_clique_(cta|pairs)" 0 5 --workload cl4
-cap cl5w16 "X=0" "k_clique_cta" 1 1 --workload cl5
-cap c4s22 "G2M_C4_STAGE_CAP=1048576" "k_c4_stage" 0 2 --workload c4 --scale 22
+case "${2:-default}" in
+  default)
+    cap cl4 "X=0" "k_clique_(cta|pairs)" 0 5 --workload cl4
+    cap cl5w16 "X=0" "k_clique_cta" 1 1 --workload cl5
+    cap c4s22 "G2M_C4_STAGE_CAP=1048576" "k_c4_stage" 0 2 --workload c4 --scale 22 ;;
+  t)
+    cap c4s24 "G2M_C4_STAGE_CAP=1048576" "k_c4_stage2" 0 1 --workload c4 --scale 24
+    cap mc4 "X=0" "g2m_plan" 0 3 --workload mc4
+    cap cl4b "X=0" "k_clique_cta" 1 1 --workload cl4 ;;
+esac
 du -sh gpurun_out
