@@ -179,12 +179,53 @@ k_c4_cta(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __
     if (lane == 0 && acc) g2m_add128(count, acc, 0);
 }
 
+// CTA-wide exclusive scan of H[0, nb) in place (every warp scans one chunk,
+// warp 0 scans the chunk totals) and the compaction of the non-empty buckets
+// into NBL (ascending), *nne of them. WT: 2 * NW words of scratch.
+template <int NW>
+__device__ __forceinline__ void cta_scan_compact(u32* H, u32 nb, u32* NBL, u32* WT, u32* nne) {
+    const u32 lane = g2m_lane();
+    const u32 w = threadIdx.x >> 5;
+    const u32 ch = ((nb + NW - 1) / NW + 31u) & ~31u;         // chunk per warp, multiple of 32
+    const u32 c0 = min(nb, w * ch), c1 = min(nb, c0 + ch);
+    u32 sum = 0, cnt = 0;
+    for (u32 b0 = c0; b0 < c1; b0 += 32) {
+        const u32 b = b0 + lane;
+        const u32 v = b < c1 ? H[b] : 0u;
+        const u32 incl = g2m_scan_incl(v);
+        sum += __shfl_sync(G2M_FULL, incl, 31);
+        cnt += __popc(__ballot_sync(G2M_FULL, v != 0u));
+    }
+    if (lane == 0) { WT[w] = sum; WT[NW + w] = cnt; }
+    __syncthreads();
+    if (w == 0) {
+        const u32 a = lane < NW ? WT[lane] : 0u, c = lane < NW ? WT[NW + lane] : 0u;
+        const u32 ia = g2m_scan_incl(a), ic = g2m_scan_incl(c);
+        if (lane < NW) { WT[lane] = ia - a; WT[NW + lane] = ic - c; }
+        if (lane == 31) *nne = ic;
+    }
+    __syncthreads();
+    u32 carry = WT[w], ccarry = WT[NW + w];
+    for (u32 b0 = c0; b0 < c1; b0 += 32) {
+        const u32 b = b0 + lane;
+        const u32 v = b < c1 ? H[b] : 0u;
+        const u32 incl = g2m_scan_incl(v);
+        const u32 m = __ballot_sync(G2M_FULL, v != 0u);
+        if (b < c1) H[b] = carry + incl - v;
+        if (v) NBL[ccarry + __popc(m & g2m_lanemask_lt())] = b;
+        carry += __shfl_sync(G2M_FULL, incl, 31);
+        ccarry += __popc(m);
+    }
+    __syncthreads();
+}
+
 // ---- tier 3: CTA per v1, bucketed staging ------------------------------------
 // Shared memory: bucket histogram -> cursors -> bucket ends [nbmax] u32 |
 // per-warp counters [NW x 1024] u32 | per-warp scratch [NW x 96] u32.
 // stage: this block's slab of stage_cap u32 in HBM.
 __host__ __device__ constexpr size_t stage_smem_bytes(int NW, u32 nbmax) {
-    return (size_t)4 * nbmax + (size_t)4 * NW * kBucketIds + (size_t)4 * NW * 96;
+    return (size_t)4 * nbmax + (size_t)4 * NW * kBucketIds + (size_t)4 * NW * 96 + (size_t)4 * nbmax +
+           (size_t)4 * 2 * NW;
 }
 
 template <int NW>
@@ -199,9 +240,11 @@ k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* 
     const u32 w = threadIdx.x >> 5;
     u32* wcnt = WC + w * kBucketIds;
     u32* wscr = WC + NW * kBucketIds + w * 96;
+    u32* NBL = WC + NW * kBucketIds + NW * 96;   // non-empty buckets [nbmax]
+    u32* WT = NBL + nbmax;                       // scan scratch [2 NW]
     u32* stage = stage_all + (u64)blockIdx.x * stage_cap;
     __shared__ u64 s_t;
-    __shared__ u32 s_row, s_row2, s_bkt;
+    __shared__ u32 s_row, s_row2, s_bkt, s_nne;
     for (u32 x = lane; x < kBucketIds; x += 32) wcnt[x] = 0;
     u64 acc = 0;
     for (;;) {
@@ -221,18 +264,10 @@ k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* 
         // 1: histogram of the wedge ends by bucket
         wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row, wscr, [&](u32 x) { atomicAdd(H + (x >> kBucketBits), 1u); });
         __syncthreads();
-        // 2: exclusive scan of the histogram (warp 0): cursors = bucket starts
-        if (w == 0) {
-            u32 carry = 0;
-            for (u32 b0 = 0; b0 < nb; b0 += 32) {
-                const u32 b = b0 + lane;
-                const u32 v = b < nb ? H[b] : 0u;
-                const u32 incl = g2m_scan_incl(v);
-                if (b < nb) H[b] = carry + incl - v;
-                carry += __shfl_sync(G2M_FULL, incl, 31);
-            }
-        }
-        __syncthreads();
+        // 2: exclusive scan of the histogram (CTA-wide): cursors = bucket starts;
+        //    the non-empty buckets listed for step 4
+        cta_scan_compact<NW>(H, nb, NBL, WT, &s_nne);
+        const u32 nne = s_nne;
         // 3: scatter the wedge ends into their buckets (cursors end as bucket ends)
         wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row2, wscr, [&](u32 x) {
             stage[atomicAdd(H + (x >> kBucketBits), 1u)] = x;
@@ -243,9 +278,9 @@ k_c4_stage(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* 
             u32 b = 0;
             if (lane == 0) b = atomicAdd(&s_bkt, 1u);
             b = __shfl_sync(G2M_FULL, b, 0);
-            if (b >= nb) break;
+            if (b >= nne) break;
+            b = NBL[b];
             const u32 s0 = b ? H[b - 1] : 0u, s1 = H[b];
-            if (s0 == s1) continue;
             for (u32 e = s0 + lane; e < s1; e += 32) acc += atomicAdd(wcnt + (stage[e] & (kBucketIds - 1)), 1u);
             __syncwarp();
             for (u32 e = s0 + lane; e < s1; e += 32) wcnt[stage[e] & (kBucketIds - 1)] = 0;
@@ -280,10 +315,12 @@ constexpr u32 kRoundKeys = kRoundBuckets * (kCoarseIds >> 10);   // (bucket, sub
 
 __host__ __device__ constexpr size_t stage2_smem_bytes(int NW, u32 nbmax) {
     return (size_t)4 * nbmax + (size_t)4 * kCoarseIds + (size_t)4 * NW * 96 + (size_t)4 * kRoundEntries +
-           (size_t)4 * (kRoundKeys + 1);
+           (size_t)4 * (kRoundKeys + 1) + (size_t)4 * nbmax + (size_t)4 * 2 * NW;
 }
 
 __device__ u32 g_c4_rounds = 1;
+
+
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
@@ -299,6 +336,9 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
     u32* wscr = C + kCoarseIds + w * 96;
     u32* RS = C + kCoarseIds + NW * 96;          // round staging [kRoundEntries]
     u32* RK = RS + kRoundEntries;                // round group cursors [kRoundKeys + 1]
+    u32* NBL = RK + kRoundKeys + 1;              // non-empty buckets [nbmax]
+    u32* WT = NBL + nbmax;                       // scan scratch [2 NW]
+    __shared__ u32 s_nne;
     u32* stage = stage_all + (u64)blockIdx.x * stage_cap;
     __shared__ u64 s_t;
     __shared__ u32 s_row, s_row2;
@@ -320,28 +360,24 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
         __syncthreads();
         wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row, wscr, [&](u32 x) { atomicAdd(H + (x >> kCoarseBits), 1u); });
         __syncthreads();
-        if (w == 0) {
-            u32 carry = 0;
-            for (u32 b0 = 0; b0 < nb; b0 += 32) {
-                const u32 b = b0 + lane;
-                const u32 v = b < nb ? H[b] : 0u;
-                const u32 incl = g2m_scan_incl(v);
-                if (b < nb) H[b] = carry + incl - v;
-                carry += __shfl_sync(G2M_FULL, incl, 31);
-            }
-        }
-        __syncthreads();
+        // CTA-wide scan (bucket starts) + the list of non-empty buckets: the count
+        // phase visits only those (a warp-0 scan and a walk over every bucket id
+        // were 38 % of the stall samples, profiles/r02/hotspots_r02t.txt)
+        cta_scan_compact<NW>(H, nb, NBL, WT, &s_nne);
+        const u32 nne = s_nne;
         wedge_rows(off, nbr, L, l1, r1, lo_x, &s_row2, wscr, [&](u32 x) {
             stage[atomicAdd(H + (x >> kCoarseBits), 1u)] = x;
         });
         __syncthreads();
-        for (u32 b = 0; b < nb;) {
+        for (u32 k = 0; k < nne;) {
+            const u32 b = NBL[k];
             const u32 s0 = b ? H[b - 1] : 0u, s1 = H[b];
-            if (s0 == s1) { ++b; continue; }
             if (g_c4_rounds && s1 - s0 <= kRoundEntries) {
-                // a round: buckets [b, be) with <= kRoundEntries entries in total
-                u32 be = b + 1;
-                while (be < nb && be - b < kRoundBuckets && H[be] - s0 <= kRoundEntries) ++be;
+                // a round: non-empty buckets NBL[k, ke) within kRoundBuckets ids of b,
+                // <= kRoundEntries entries in total; they end at bucket be - 1
+                u32 ke = k + 1;
+                while (ke < nne && NBL[ke] - b < kRoundBuckets && H[NBL[ke]] - s0 <= kRoundEntries) ++ke;
+                const u32 be = NBL[ke - 1] + 1;
                 const u32 tot = H[be - 1] - s0;
                 const u32 nkey = (be - b) << (kCoarseBits - 10);
                 for (u32 x = threadIdx.x; x <= nkey; x += NT) RK[x] = 0;
@@ -382,7 +418,7 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
                     __syncwarp();
                 }
                 __syncthreads();
-                b = be;
+                k = ke;
                 continue;
             }
             for (u32 e = s0 + threadIdx.x; e < s1; e += NT) acc += atomicAdd(C + (stage[e] & (kCoarseIds - 1)), 1u);
@@ -393,7 +429,7 @@ k_c4_stage2(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32*
                 for (u32 e = s0 + threadIdx.x; e < s1; e += NT) C[stage[e] & (kCoarseIds - 1)] = 0;
             }
             __syncthreads();
-            ++b;
+            ++k;
         }
     }
     acc = g2m_wsum(acc);
