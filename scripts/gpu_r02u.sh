@@ -1,0 +1,7 @@
+# round 2: 4-cycle CTA-wide scan + non-empty bucket list (tests + timing RMAT-24/25/27)
+mkdir -p gpurun_out
+T=${1:-r02u}
+timeout 600 python -m pytest tests -m gpu -q -x -k "cycle4 or c4" > gpurun_out/${T}_pytest.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/${T}_pytest.log
+AB_REPS=2 timeout 900 python scripts/ab_env.py 24 c4 "X=0" debug > gpurun_out/${T}_c424.txt 2>&1; echo c424 rc=$?; grep -E "c4 \[|cycle4" gpurun_out/${T}_c424.txt | head -8
+AB_REPS=1 timeout 900 python scripts/ab_env.py 25 c4 "X=0" debug > gpurun_out/${T}_c425.txt 2>&1; echo c425 rc=$?; grep -E "c4 \[|cycle4" gpurun_out/${T}_c425.txt | head -8
+AB_REPS=1 timeout 1200 python scripts/ab_env.py 27 c4 "X=0" debug > gpurun_out/${T}_c427.txt 2>&1; echo c427 rc=$?; grep -E "c4 \[|cycle4" gpurun_out/${T}_c427.txt | head -8
