@@ -523,95 +523,6 @@ __global__ void k_c4_sweep(u32* dense, u64 n, u64* count) {
     if ((threadIdx.x & 31) == 0 && acc) g2m_add128(count, acc, 0);
 }
 
-// ---- tier 4, grid-staged (G2M_C4_GSTAGE): one top vertex on the whole grid.
-// Its wedge ends are bucketed by 32K-id range into a grid-wide slab -- a
-// histogram walk and a scatter walk over the flattened row segments, with one
-// global atomic per sorted run of a warp's ends (a hub's rows are long and
-// sorted, so a 32-lane step mostly shares one bucket) -- then every bucket is
-// counted by one CTA in dense shared counters: shared atomics instead of the
-// L2 reductions of the range passes.
-
-// Warp-collective append of a warp's bucket ids b (valid lanes a prefix): one
-// atomic per run of equal b; returns each valid lane's slot.
-__device__ __forceinline__ u32 run_append(u32* H, u32 b, bool v) {
-    const u32 lane = g2m_lane();
-    const u32 pb = __shfl_up_sync(G2M_FULL, b, 1);
-    const u32 vm = __ballot_sync(G2M_FULL, v);
-    const bool start = v && (lane == 0 || pb != b);
-    const u32 sm = __ballot_sync(G2M_FULL, start);
-    const u32 vend = 32u - (u32)__clz(vm);
-    u32 base = 0;
-    if (start) {
-        const u32 higher = lane == 31 ? 0u : (sm & ~((2u << lane) - 1u));
-        const u32 end = higher ? (u32)(__ffs(higher) - 1) : vend;
-        base = atomicAdd(H + b, end - lane);
-    }
-    const u32 below = sm & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
-    const u32 rs = below ? 31u - (u32)__clz(below) : 0u;
-    base = __shfl_sync(G2M_FULL, base, rs);
-    return base + lane - rs;
-}
-
-template <bool SCATTER>
-__global__ void __launch_bounds__(512)
-k_c4_gwalk(const u32* __restrict__ nbr, u32 l1, const u64* __restrict__ rb, const u64* __restrict__ re, u64* ctr,
-           u32 lo, u32* hist, u32* slab) {
-    const u32 lane = g2m_lane();
-    const u64 tot = re[l1 - 1];
-    for (;;) {
-        u64 e0 = 0;
-        if (lane == 0) e0 = atomicAdd(ctr, 1024ull);
-        e0 = __shfl_sync(G2M_FULL, e0, 0);
-        if (e0 >= tot) break;
-        u32 ow = 0, n = l1;
-        while (n > 0) {
-            const u32 h = n >> 1;
-            if (__ldg(re + ow + h) <= e0) { ow += h + 1; n -= h + 1; } else n = h;
-        }
-        for (u32 k = 0; k < 1024; k += 32) {
-            const u64 e = e0 + k + lane;
-            const bool v = e < tot;
-            u32 x = 0;
-            if (v) {
-                while (__ldg(re + ow) <= e) ++ow;
-                x = __ldg(nbr + __ldg(rb + ow) + e);
-            }
-            const u32 slot = run_append(hist, v ? (x - lo) >> kCoarseBits : 0u, v);
-            if (SCATTER && v) slab[slot] = x;
-        }
-    }
-}
-
-template <int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
-k_c4_gcount(const u32* __restrict__ slab, const u32* __restrict__ hend, u32 nbk, u32 lo, u64* bctr, u64* count) {
-    extern __shared__ __align__(16) u32 smem_c4[];
-    constexpr u32 NT = NW * 32;
-    u32* C = smem_c4;
-    __shared__ u32 s_b;
-    for (u32 x = threadIdx.x; x < kCoarseIds; x += NT) C[x] = 0;
-    u64 acc = 0;
-    for (;;) {
-        if (threadIdx.x == 0) s_b = (u32)atomicAdd(bctr, 1ull);
-        __syncthreads();
-        const u32 b = s_b;
-        if (b >= nbk) break;
-        const u32 s0 = b ? hend[b - 1] : 0u, s1 = hend[b];
-        if (s0 != s1) {
-            for (u32 e = s0 + threadIdx.x; e < s1; e += NT) acc += atomicAdd(C + ((slab[e] - lo) & (kCoarseIds - 1)), 1u);
-            __syncthreads();
-            if (s1 - s0 > kCoarseIds / 4) {
-                for (u32 x = threadIdx.x; x < kCoarseIds; x += NT) C[x] = 0;
-            } else {
-                for (u32 e = s0 + threadIdx.x; e < s1; e += NT) C[(slab[e] - lo) & (kCoarseIds - 1)] = 0;
-            }
-        }
-        __syncthreads();
-    }
-    acc = g2m_wsum(acc);
-    if (g2m_lane() == 0 && acc) g2m_add128(count, acc, 0);
-}
-
 // Per v1 (rank r, this partition): l1 = |N(r) ∩ [0, r)| and the wedge bound
 // W = Σ_{v ∈ N<(r)} d(v); class 1..4 as above (0: l1 < 2, no cycle).
 // One warp per vertex.

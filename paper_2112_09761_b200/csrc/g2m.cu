@@ -172,7 +172,6 @@ struct DevState {
     DevBuf counters;    // next, counts, stats
     DevBuf scratch;     // per-warp slots
     DevBuf tasks_a, tasks_b, task_match, matches, cub_tmp;
-    DevBuf c4gslab, c4ghist;    // 4-cycle grid-staged tier: slab, bucket counts + cursors
     int sms = 0;
     uint64_t launches = 0;   // kernels of ours launched on this device (g2m_run_stats.launches)
     DevBuf tmp1, tmp2;       // grow-only scratch of the preprocessing passes (rank relabelling)
@@ -2831,66 +2830,10 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
         G2M_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, rn, re, (int64_t)lmax, st->stream));
         G2M_TRY(st->cub_tmp.ensure(tb));
         G2M_CUDA(cudaMemsetAsync(dense, 0, range * 4, st->stream));
-        // G2M_C4_GSTAGE=1: a top vertex whose whole fan fits the slab is bucketed
-        // into it by the whole grid and counted per 32K-id bucket in shared memory
-        // (k_c4_gwalk / k_c4_gcount); bigger fans take the range passes below
-        const bool gstage = getenv("G2M_C4_GSTAGE") && atoi(getenv("G2M_C4_GSTAGE")) != 0;
-        u64 slab_cap = 0;
-        u32* hist = nullptr;
-        u32* hcur = nullptr;
-        size_t tbh = 0;
-        constexpr int NWC = 32;
-        if (gstage) {
-            size_t fr = 0, tot_b = 0;
-            cudaMemGetInfo(&fr, &tot_b);
-            slab_cap = std::min<u64>((u64)0xffffffffull, (fr / 3) / 4);
-            G2M_TRY(st->c4gslab.ensure(slab_cap * 4));
-            const u64 nbk_max = ((u64)(stride - lo_x) >> g2m_c4::kCoarseBits) + 2;
-            G2M_TRY(st->c4ghist.ensure(nbk_max * 8 + 64));
-            hist = st->c4ghist.as<u32>();
-            hcur = hist + nbk_max;
-            G2M_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tbh, hist, hcur, (int64_t)nbk_max, st->stream));
-            G2M_TRY(st->cub_tmp.ensure(std::max(tb, tbh)));
-            G2M_CUDA(cudaFuncSetAttribute(g2m_c4::k_c4_gcount<NWC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)(4 * g2m_c4::kCoarseIds)));
-        }
-        u64 passes = 0, gstaged = 0;
+        u64 passes = 0;
         G2M_TRY(timed([&]() -> int {
             for (u64 q = 0; q < sizes[4]; ++q) {
                 const u32 r1 = gv[q], l1 = gl[q];
-                if (gstage) {
-                    // row segments of the whole fan [lo_x, r1)
-                    ++st->launches;
-                    g2m_c4::k_c4_rows<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(off, nbr, r1, l1, lo_x, r1, rn, rb);
-                    size_t t2 = tb;
-                    G2M_CUDA(cub::DeviceScan::InclusiveSum(st->cub_tmp.p, t2, rn, re, (int64_t)l1, st->stream));
-                    ++st->launches;
-                    g2m_c4::k_c4_base<<<grid_for(st, l1, 256), 256, 0, st->stream>>>(l1, rn, rb, re);
-                    uint64_t wtot = 0;
-                    G2M_CUDA(cudaMemcpyAsync(&wtot, re + l1 - 1, 8, cudaMemcpyDeviceToHost, st->stream));
-                    G2M_CUDA(cudaStreamSynchronize(st->stream));
-                    if (wtot <= slab_cap) {
-                        ++gstaged;
-                        const u32 nbk = ((r1 - lo_x) >> g2m_c4::kCoarseBits) + 1;
-                        G2M_CUDA(cudaMemsetAsync(hist, 0, (size_t)nbk * 4, st->stream));
-                        G2M_CUDA(cudaMemsetAsync(gctr, 0, 8, st->stream));
-                        ++st->launches;
-                        g2m_c4::k_c4_gwalk<false><<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rb, re, gctr, lo_x,
-                                                                                       hist, nullptr);
-                        size_t t3 = tbh;
-                        G2M_CUDA(cub::DeviceScan::ExclusiveSum(st->cub_tmp.p, t3, hist, hcur, (int64_t)nbk, st->stream));
-                        G2M_CUDA(cudaMemsetAsync(gctr, 0, 8, st->stream));
-                        ++st->launches;
-                        g2m_c4::k_c4_gwalk<true><<<st->sms * 4, 512, 0, st->stream>>>(nbr, l1, rb, re, gctr, lo_x,
-                                                                                      hcur, st->c4gslab.as<u32>());
-                        G2M_CUDA(cudaMemsetAsync(gctr, 0, 8, st->stream));
-                        ++st->launches;
-                        g2m_c4::k_c4_gcount<NWC><<<st->sms, NWC * 32, 4 * g2m_c4::kCoarseIds, st->stream>>>(
-                            st->c4gslab.as<u32>(), hcur, nbk, lo_x, gctr, count);
-                        G2M_CUDA(cudaGetLastError());
-                        continue;
-                    }
-                }
                 for (u64 lo = lo_x; lo < r1; lo += range) {
                     const u32 hi = (u32)std::min<u64>(r1, lo + range);
                     ++passes;
@@ -2920,9 +2863,8 @@ static int cycle4_impl(const g2m_graph* g, const g2m_task_spec* part, uint64_t* 
             }
             return G2M_OK;
         }));
-        if (dbg) fprintf(stderr, "[g2m] cycle4 grid tier: %llu sources (%llu grid-staged), %llu range passes of <= %llu ids\n",
-                         (unsigned long long)sizes[4], (unsigned long long)gstaged, (unsigned long long)passes,
-                         (unsigned long long)range);
+        if (dbg) fprintf(stderr, "[g2m] cycle4 grid tier: %llu sources, %llu range passes of <= %llu ids\n",
+                         (unsigned long long)sizes[4], (unsigned long long)passes, (unsigned long long)range);
     }
     uint64_t h[2] = {0, 0};
     G2M_CUDA(cudaMemcpyAsync(h, count, 16, cudaMemcpyDeviceToHost, st->stream));

@@ -155,7 +155,7 @@ def test_kernel_work_counters(monkeypatch):
 
 
 @pytest.mark.parametrize("rng_ids", ["2048", "100000"])
-@pytest.mark.parametrize("red", ["0", "1", "gstage"])
+@pytest.mark.parametrize("red", ["0", "1"])
 def test_cycle4_grid_tier_range_passes(monkeypatch, rng_ids, red):
     # every top vertex through the grid tier, its wedge ends counted over
     # several id ranges (the n > L2 design of RMAT-27)
@@ -165,10 +165,7 @@ def test_cycle4_grid_tier_range_passes(monkeypatch, rng_ids, red):
     want = EX.execute(g, f, tasks, lgs=False)[0]
     monkeypatch.setenv("G2M_C4_STAGE_CAP", "0")
     monkeypatch.setenv("G2M_C4_RANGE", rng_ids)
-    if red == "gstage":
-        monkeypatch.setenv("G2M_C4_GSTAGE", "1")
-    else:
-        monkeypatch.setenv("G2M_C4_RED", red)
+    monkeypatch.setenv("G2M_C4_RED", red)
     g2 = GR.from_edges(G.rmat_edges(13, 16, 3), num_vertices=1 << 13)
     got = EX.execute(g2, f, EX._default_tasks(g2, f))[0]
     assert got == want
