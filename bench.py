@@ -42,7 +42,7 @@ of the reference executor) with all host threads on a bounded task sample.
 from __future__ import annotations
 
 import argparse
-import gc
+import gc as pygc
 import json
 import os
 import socket
@@ -556,7 +556,7 @@ def main():
             del hg
             # the previous call's graphs (and their device replicas) go before the
             # next timed call, not at some later cyclic-GC pass inside it
-            gc.collect()
+            pygc.collect()
             if i >= nw:
                 e2e_s.append(dt)
         log("e2e steps ms", [round(x * 1000.0, 1) for x in e2e_s])
