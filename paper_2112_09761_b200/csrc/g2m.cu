@@ -23,6 +23,7 @@
 #include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -172,6 +173,9 @@ struct DevState {
     DevBuf counters;    // next, counts, stats
     DevBuf scratch;     // per-warp slots
     DevBuf tasks_a, tasks_b, task_match, matches, cub_tmp;
+    DevBuf core_bits;           // hub core of graph core_gid (see ensure_core)
+    uint64_t core_gid = 0;
+    uint32_t core_lo = 0, core_T = 0;
     int sms = 0;
     uint64_t launches = 0;   // kernels of ours launched on this device (g2m_run_stats.launches)
     DevBuf tmp1, tmp2;       // grow-only scratch of the preprocessing passes (rank relabelling)
@@ -233,7 +237,10 @@ static int dev_state(int dev, DevState** out) {
 // graph
 // ---------------------------------------------------------------------------
 
+static std::atomic<uint64_t> g_graph_ids{1};
+
 struct g2m_graph {
+    const uint64_t gid = g_graph_ids.fetch_add(1);   // identity for per-device caches
     int dev = 0;
     uint64_t nv = 0, slots = 0, maxdeg = 0, sumsq = 0;
     int oriented = 0;
@@ -260,9 +267,8 @@ struct g2m_graph {
     // id of the first owned vertex (owned vertices are consecutive)
     DevBuf l2g;
     uint64_t part_first = 0, part_owned = 0;
-    // oriented graphs: the hub core of the rank-space DAG (g2m_clique::HubCore)
-    DevBuf core_bits;
-    uint32_t core_lo = 0, core_T = 0;
+    // oriented graphs: the hub core lives in the device state (one per device,
+    // rebuilt when another graph uses it: no per-graph GB-sized allocations)
 };
 
 // out[0] = max degree, out[1] = Σ degree² (the BFS frontier bound, executor.choose_search)
@@ -1312,27 +1318,27 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
 // rows (profiles/r02/core_ab.txt, ctacore_ab.txt); 0 = off.
 static g2m_clique::HubCore ensure_core(const g2m_graph* cg, DevState* st) {
     g2m_graph* g = const_cast<g2m_graph*>(cg);
-    std::lock_guard<std::mutex> lk(g->mu);
     g2m_clique::HubCore hc{nullptr, 0, 0};
     const char* e = getenv("G2M_PAIR_CORE");
     const int lg = e ? atoi(e) : 17;
     if (lg <= 0 || !g->oriented || !g->has_rank || g->rk_down || g->nv < 2) return hc;
     const u64 T = std::min<u64>((u64)1 << std::min(lg, 20), g->nv);
-    if (g->core_T != T) {
+    if (st->core_gid != g->gid || st->core_T != T) {
         const u64 q = (T - 1) >> 5, r = (T - 1) & 31u;
         const u64 words = 16ull * q * (q + 1) + r * (q + 1) + 1;
-        if (g->core_bits.ensure(words * 4) != G2M_OK) { cudaGetLastError(); return hc; }
-        cudaMemsetAsync(g->core_bits.p, 0, words * 4, st->stream);
-        g->core_lo = (uint32_t)(g->nv - T);
+        if (st->core_bits.ensure(words * 4) != G2M_OK) { cudaGetLastError(); st->core_gid = 0; return hc; }
+        cudaMemsetAsync(st->core_bits.p, 0, words * 4, st->stream);
+        st->core_lo = (uint32_t)(g->nv - T);
         ++st->launches;
         g2m_clique::k_core_build<<<grid_for(st, T * 32, 256), 256, 0, st->stream>>>(
-            g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), g->nv, g->core_lo, (u32)T, g->core_bits.as<u32>());
-        if (cudaGetLastError() != cudaSuccess) return hc;
-        g->core_T = (uint32_t)T;
+            g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), g->nv, st->core_lo, (u32)T, st->core_bits.as<u32>());
+        if (cudaGetLastError() != cudaSuccess) { st->core_gid = 0; return hc; }
+        st->core_T = (uint32_t)T;
+        st->core_gid = g->gid;
     }
-    hc.bits = g->core_bits.as<u32>();
-    hc.lo = g->core_lo;
-    hc.T = g->core_T;
+    hc.bits = st->core_bits.as<u32>();
+    hc.lo = st->core_lo;
+    hc.T = st->core_T;
     return hc;
 }
 
