@@ -173,6 +173,7 @@ struct DevState {
     DevBuf counters;    // next, counts, stats
     DevBuf scratch;     // per-warp slots
     DevBuf tasks_a, tasks_b, task_match, matches, cub_tmp;
+    DevBuf gr_slab;             // rows of the clique tiers that keep them in L2
     DevBuf core_bits;           // hub core of graph core_gid (see ensure_core)
     uint64_t core_gid = 0;
     uint32_t core_lo = 0, core_T = 0;
@@ -2191,7 +2192,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
     G2M_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
     int sm_smem = 0;
     G2M_CUDA(cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0));
-    DevBuf slab;   // global rows of the GR tier
+    DevBuf& slab = st->gr_slab;   // global rows of the GR tier (grow-only, per device)
     // G2M_DIRECT_MAX: widest window (bits) for the direct bitmap (tests force
     // the two-level window / hash paths with small values)
     const u32 direct_max = getenv("G2M_DIRECT_MAX") ? (u32)strtoul(getenv("G2M_DIRECT_MAX"), nullptr, 10)
@@ -2312,7 +2313,7 @@ static int clique_launch_all(const u64* off, const u32* nbr, DevState* st, const
         }));
         ++slot;
     }
-    return join();   // before `slab` (used on a side stream) is released on the main stream
+    return join();
 }
 
 // ---- pattern-aware workload estimator ----
