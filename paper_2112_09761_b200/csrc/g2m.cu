@@ -183,6 +183,7 @@ struct DevState {
     DevBuf frontier;         // BFS level-3 frontier items (grow-only)
     DevBuf c4slab;           // 4-cycle staging slabs, one per block
     DevBuf hubs;             // [0] = count, then the hub rows of a row pass (rows longer than kHubRow)
+    DevBuf mids;             // the same for the orientation's mid-length rows
     // side streams: independent kernel tiers run concurrently so one tier's
     // tail overlaps the next tier's work (fork/join through events)
     static constexpr int kSide = 8;
@@ -253,6 +254,10 @@ struct g2m_graph {
     // the same graph relabelled by its (degree, id) order, lazily built
     DevBuf rk_off, rk_nbr;
     bool has_rank = false;
+    // oriented graphs built by g2m_graph_orient: the undirected degree of every
+    // vertex (the orientation's key), so the rank order needs no in-degree pass
+    DevBuf symdeg;
+    uint64_t symdeg_max = 0;
     uint64_t rk_deg1 = 0;    // ranks [0, rk_deg1) have degree <= 1
     // oriented graphs: rank-space rows holding a column <= their row, i.e. DAG
     // edges against the (degree, id) order (an input oriented some other way)
@@ -420,13 +425,20 @@ __device__ __forceinline__ void push_hub(u32* hubs, u32 u) {
     hubs[1 + atomicAdd(hubs, 1u)] = u;
 }
 
-// Block-wide sum (kHubThreads threads); result valid in every thread.
+// Orientation passes: rows of kOrientMid < d <= kHubRow (clustered at the low
+// ids of a skewed graph, so 32 of them would queue on one warp) get one
+// kOrientMidThreads CTA each, several CTAs per SM.
+constexpr u32 kOrientMid = 64;
+constexpr int kOrientMidThreads = 256;
+
+// Block-wide sum (NT threads); result valid in every thread.
+template <int NT = kHubThreads>
 __device__ __forceinline__ u64 block_sum_hub(u64 v, u64* red) {
     v = g2m_wsum(v);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
     u64 t = 0;
-    for (int w = 0; w < kHubThreads / 32; ++w) t += red[w];
+    for (int w = 0; w < NT / 32; ++w) t += red[w];
     __syncthreads();
     return t;
 }
@@ -440,7 +452,7 @@ __device__ __forceinline__ u64 keep_word(u64 b, u64 u, u64 base) { return (b >> 
 // Light rows in groups of 32: lane j fetches row v0 + j's offsets, then the
 // warp walks the group's rows (one dependent load less per row).
 __global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u64 nv, u64* cnt, u32* hubs,
-                               u32* keep) {
+                               u32* keep, u32* mids, u32 mid) {
     const u32 lane = g2m_lane();
     for (u64 v0 = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; v0 < nv;
          v0 += (((u64)gridDim.x * blockDim.x) >> 5) * 32) {
@@ -457,8 +469,8 @@ __global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u
             const u64 b = __shfl_sync(G2M_FULL, bl, j), e = __shfl_sync(G2M_FULL, el, j);
             const u32 u = (u32)(v0 + j);
             const u32 du = (u32)(e - b);
-            if (du > kHubRow) {
-                if (lane == 0) push_hub(hubs, u);
+            if (du > mid) {
+                if (lane == 0) push_hub(du > kHubRow ? hubs : mids, u);
                 continue;
             }
             u32 c = 0;
@@ -473,13 +485,15 @@ __global__ void k_orient_count(const u64* off, const u32* nbr, const u32* deg, u
             }
             if (lane == j) mycnt = c;
         }
-        // hub rows are overwritten by k_orient_count_hubs
+        // hub / mid rows are overwritten by k_orient_count_hubs
         if (vl < nv) cnt[vl] = mycnt;
     }
 }
 
-__global__ void __launch_bounds__(kHubThreads)
+template <int NT>
+__global__ void __launch_bounds__(NT)
 k_orient_count_hubs(const u64* off, const u32* nbr, const u32* deg, const u32* hubs, u64* cnt, u32* keep) {
+    constexpr int kHubThreads = NT;
     __shared__ u64 red[kHubThreads / 32];
     const u32 nh = hubs[0];
     const u32 lane = g2m_lane(), wid = threadIdx.x >> 5;
@@ -496,12 +510,13 @@ k_orient_count_hubs(const u64* off, const u32* nbr, const u32* deg, const u32* h
             if (lane == 0 && base + 32 * wid < e) keep[keep_word(b, u, base + 32 * wid)] = m;
             c += k ? 1 : 0;
         }
-        c = block_sum_hub(c, red);
+        c = block_sum_hub<NT>(c, red);
         if (threadIdx.x == 0) cnt[u] = c;
     }
 }
 
-__global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* keep, u64 nv, const u64* noff, u32* out) {
+__global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* keep, u64 nv, const u64* noff, u32* out,
+                              u32 mid) {
     const u32 lane = g2m_lane();
     for (u64 v0 = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; v0 < nv;
          v0 += (((u64)gridDim.x * blockDim.x) >> 5) * 32) {
@@ -512,7 +527,7 @@ __global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* keep, u
             el = off[vl + 1];
             wl = noff[vl];
         }
-        const u32 light = __ballot_sync(G2M_FULL, el > bl && el - bl <= kHubRow);   // hubs: k_orient_fill_hubs
+        const u32 light = __ballot_sync(G2M_FULL, el > bl && el - bl <= mid);   // others: k_orient_fill_hubs
         for (u32 todo = light; todo; todo &= todo - 1) {
             const u32 j = __ffs(todo) - 1;
             const u64 b = __shfl_sync(G2M_FULL, bl, j), e = __shfl_sync(G2M_FULL, el, j);
@@ -529,8 +544,10 @@ __global__ void k_orient_fill(const u64* off, const u32* nbr, const u32* keep, u
 
 // Ordered compaction of a hub row: 1024-slot steps, warp ballots, warp
 // offsets from a shared prefix.
-__global__ void __launch_bounds__(kHubThreads)
+template <int NT>
+__global__ void __launch_bounds__(NT)
 k_orient_fill_hubs(const u64* off, const u32* nbr, const u32* keep, const u32* hubs, const u64* noff, u32* out) {
+    constexpr int kHubThreads = NT;
     __shared__ u32 wc[kHubThreads / 32];
     const u32 lane = g2m_lane(), wid = threadIdx.x >> 5;
     const u32 nh = hubs[0];
@@ -596,8 +613,11 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     };
     G2M_TRY(o->off.ensure((g->nv + 1) * 8));
     DevBuf& cnt = st->tmp1;   // grow-only scratch (the caller holds the device lock)
-    DevBuf& deg = st->tmp2;
+    DevBuf& deg = o->symdeg;   // kept: the rank order of the oriented graph reuses it
+    o->symdeg_max = g->maxdeg;
     u32* hubs = nullptr;
+    u32* mids = nullptr;
+    const u32 mid = getenv("G2M_ORIENT_MID") ? (u32)std::max(32, atoi(getenv("G2M_ORIENT_MID"))) : kOrientMid;
     DevBuf keep;   // keep ballots of the count pass
     G2M_TRY(keep.ensure(((g->slots >> 5) + g->nv + 2) * 4));
     G2M_TRY(cnt.ensure(std::max<uint64_t>(g->nv, 1) * 8));
@@ -607,11 +627,16 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
         k_degrees<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, deg.as<u32>());
         int grid = grid_for(st, g->nv * 32, 256);
         G2M_TRY(hub_list(st, g->slots, kHubRow, &hubs));
-        st->launches += 2;
+        G2M_TRY(st->mids.ensure((g->slots / (mid + 1) + 2) * 4));
+        mids = st->mids.as<u32>();
+        G2M_CUDA(cudaMemsetAsync(mids, 0, 4, st->stream));
+        st->launches += 3;
         k_orient_count<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv,
-                                                      cnt.as<u64>(), hubs, keep.as<u32>());
-        k_orient_count_hubs<<<hub_grid(st, g->slots), kHubThreads, 0, st->stream>>>(
+                                                      cnt.as<u64>(), hubs, keep.as<u32>(), mids, mid);
+        k_orient_count_hubs<kHubThreads><<<hub_grid(st, g->slots), kHubThreads, 0, st->stream>>>(
             g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), hubs, cnt.as<u64>(), keep.as<u32>());
+        k_orient_count_hubs<kOrientMidThreads><<<st->sms * 8, kOrientMidThreads, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), mids, cnt.as<u64>(), keep.as<u32>());
         G2M_CUDA(cudaGetLastError());
     }
     phase("degrees+count");
@@ -622,11 +647,13 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     G2M_TRY(o->nbr.ensure(std::max<uint64_t>(o->slots, 1) * 4));
     if (g->nv) {
         int grid = grid_for(st, g->nv * 32, 256);
-        st->launches += 2;
+        st->launches += 3;
         k_orient_fill<<<grid, 256, 0, st->stream>>>(g->off.as<u64>(), g->nbr.as<u32>(), keep.as<u32>(), g->nv,
-                                                     o->off.as<u64>(), o->nbr.as<u32>());
-        k_orient_fill_hubs<<<hub_grid(st, g->slots), kHubThreads, 0, st->stream>>>(
+                                                     o->off.as<u64>(), o->nbr.as<u32>(), mid);
+        k_orient_fill_hubs<kHubThreads><<<hub_grid(st, g->slots), kHubThreads, 0, st->stream>>>(
             g->off.as<u64>(), g->nbr.as<u32>(), keep.as<u32>(), hubs, o->off.as<u64>(), o->nbr.as<u32>());
+        k_orient_fill_hubs<kOrientMidThreads><<<st->sms * 8, kOrientMidThreads, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), keep.as<u32>(), mids, o->off.as<u64>(), o->nbr.as<u32>());
         G2M_CUDA(cudaGetLastError());
     }
     if (g->labels.p) {
@@ -1048,6 +1075,11 @@ __global__ void k_rank_keys(const u64* off, const u32* indeg, u64 nv, u64* keys)
         keys[v] = ((off[v + 1] - off[v] + (u64)indeg[v]) << 32) | v;
 }
 
+__global__ void k_rank_keys_sym(const u32* deg, u64 nv, u64* keys) {
+    for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < nv; v += (u64)gridDim.x * blockDim.x)
+        keys[v] = ((u64)deg[v] << 32) | v;
+}
+
 __global__ void k_count_deg_le1(const u64* keys, u64 nv, u64* out) {
     u64 c = 0;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nv; i += (u64)gridDim.x * blockDim.x)
@@ -1095,11 +1127,11 @@ k_rank_keys64_hubs(const u64* off, const u32* nbr, const u32* rank, int rb, u64*
 
 // ---- per-row rank-space fill + sort (replaces the global key sort) --------
 // Row r = rank[v] of the rank-space CSR holds rank[w] for w in N(v), sorted.
-// Rows of <= 32 are sorted in registers (warp bitonic), rows of <= 1024 in a
-// per-warp shared buffer, longer rows by one 1024-thread block per row in
-// shared memory (<= kRowSortBlock); graphs with longer rows take the global
-// key sort instead.
-constexpr u32 kRowSortWarp = 1024;
+// Rows of <= 32 are sorted in registers (warp bitonic), rows of <= 128 in a
+// per-warp shared buffer, longer rows by one 256-thread CTA per row in
+// shared memory (<= kRowSortBlock; RMAT-22 rank rows 4.1 ms with rows up to
+// 1024 on the warps); graphs with longer rows take the global key sort.
+constexpr u32 kRowSortMid = 128;    // longer rows: one CTA per row
 constexpr u32 kRowSortBlock = 8192;
 constexpr int kFillWarps = 8;
 
@@ -1133,8 +1165,9 @@ __device__ __forceinline__ void bitonic_smem(u32* s, u32 P, u32 t, u32 nt, Sync&
 }
 
 __global__ void __launch_bounds__(kFillWarps * 32)
-k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* rk_off, u32* rk_nbr, u32* hubs) {
-    __shared__ u32 buf[kFillWarps][kRowSortWarp];
+k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* rk_off, u32* rk_nbr, u32* hubs,
+            u32 mid) {
+    __shared__ u32 buf[kFillWarps][kRowSortMid];
     const u32 lane = g2m_lane();
     u32* sb = buf[threadIdx.x >> 5];
     // rows in groups of 32: each lane fetches one row's offsets and its
@@ -1154,7 +1187,7 @@ k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* 
             const u64 b = __shfl_sync(G2M_FULL, bl, j);
             const u32 d = (u32)__shfl_sync(G2M_FULL, dl, j);
             u32* out = rk_nbr + __shfl_sync(G2M_FULL, ol, j);
-            if (d > kRowSortWarp) {
+            if (d > mid) {   // one CTA per row (k_rank_fill_hubs): no warp serialises them
                 if (lane == 0) push_hub(hubs, (u32)(v0 + j));
                 continue;
             }
@@ -1174,8 +1207,13 @@ k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* 
     }
 }
 
-__global__ void __launch_bounds__(kHubThreads)
+// Rows longer than the warp threshold, one 256-thread CTA per row (several
+// CTAs per SM): the rows of a 32-row group no longer queue on one warp (the
+// long rows of a skewed graph sit together at the low original ids).
+constexpr int kRankFillThreads = 256;
+__global__ void __launch_bounds__(kRankFillThreads)
 k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_off, u32* rk_nbr, const u32* hubs) {
+    constexpr u32 kHubThreads = kRankFillThreads;
     __shared__ u32 sb[kRowSortBlock];
     const u32 nh = hubs[0];
     for (u32 h = blockIdx.x; h < nh; h += gridDim.x) {
@@ -1231,17 +1269,26 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     G2M_TRY(sorted.ensure(std::max<u64>(nv, 1) * 8));
     G2M_TRY(rank.ensure(std::max<u64>(nv, 1) * 4));
     G2M_TRY(rdeg.ensure(std::max<u64>(nv, 1) * 8));
-    G2M_CUDA(cudaMemsetAsync(indeg.p, 0, std::max<u64>(nv, 1) * 4, st->stream));
+    // an oriented graph from g2m_graph_orient carries the undirected degrees its
+    // orientation used (no in-degree atomics); others: deg = d+ + d- (symmetric
+    // graphs: the row length)
+    const bool sym = g->oriented && g->symdeg.p && !getenv("G2M_RANK_INDEG");
+    if (!sym) G2M_CUDA(cudaMemsetAsync(indeg.p, 0, std::max<u64>(nv, 1) * 4, st->stream));
     if (nv) {
-        if (slots && g->oriented) {   // symmetric graphs: deg = row length, no in-degree term
+        if (slots && g->oriented && !sym) {
             ++st->launches;
             k_rank_indeg<<<grid_for(st, slots, 256), 256, 0, st->stream>>>(g->nbr.as<u32>(), slots, indeg.as<u32>());
         }
         ++st->launches;
-        k_rank_keys<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), indeg.as<u32>(), nv, keys.as<u64>());
+        if (sym)
+            k_rank_keys_sym<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->symdeg.as<u32>(), nv, keys.as<u64>());
+        else
+            k_rank_keys<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), indeg.as<u32>(), nv,
+                                                                        keys.as<u64>());
         G2M_CUDA(cudaGetLastError());
+        const u64 dmax = sym ? g->symdeg_max : 2 * std::max<u64>(slots, 1);
         int hi = 32;
-        while (hi < 64 && ((u64)1 << (hi - 32)) <= 2 * std::max<u64>(slots, 1)) ++hi;   // degree < 2^(hi-32)
+        while (hi < 64 && ((u64)1 << (hi - 32)) <= dmax) ++hi;   // degree < 2^(hi-32)
         size_t tb = 0;
         G2M_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.as<u64>(), sorted.as<u64>(), (int64_t)nv, 0, hi,
                                                 st->stream));
@@ -1265,11 +1312,13 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     // sort (a segmented sort leaves a 10^6-slot hub row to one CTA)
     if (nv && slots && g->maxdeg <= kRowSortBlock && !getenv("G2M_RANK_RADIX")) {
         u32* hubs = nullptr;
-        G2M_TRY(hub_list(st, slots, kRowSortWarp, &hubs));
+        const u32 mid = getenv("G2M_RANK_MID") ? (u32)atoi(getenv("G2M_RANK_MID")) : kRowSortMid;
+        G2M_TRY(hub_list(st, slots, std::min(mid, kRowSortMid), &hubs));
         st->launches += 2;
         k_rank_fill<<<grid_for(st, nv * 32, kFillWarps * 32), kFillWarps * 32, 0, st->stream>>>(
-            g->off.as<u64>(), g->nbr.as<u32>(), nv, rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs);
-        k_rank_fill_hubs<<<hub_grid(st, slots), kHubThreads, 0, st->stream>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), nv, rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs,
+            std::min(mid, kRowSortMid));
+        k_rank_fill_hubs<<<st->sms * 6, kRankFillThreads, 0, st->stream>>>(
             g->off.as<u64>(), g->nbr.as<u32>(), rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs);
         G2M_CUDA(cudaGetLastError());
     } else if (nv && slots) {
