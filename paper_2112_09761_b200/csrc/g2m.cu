@@ -183,6 +183,7 @@ struct DevState {
     DevBuf frontier;         // BFS level-3 frontier items (grow-only)
     DevBuf c4slab;           // 4-cycle staging slabs, one per block
     DevBuf hubs;             // [0] = count, then the hub rows of a row pass (rows longer than kHubRow)
+    DevBuf mids;             // a second row list (rank-space rows: the CTA-sorted ones)
     // side streams: independent kernel tiers run concurrently so one tier's
     // tail overlaps the next tier's work (fork/join through events)
     static constexpr int kSide = 8;
@@ -1078,27 +1079,15 @@ k_rank_keys64_hubs(const u64* off, const u32* nbr, const u32* rank, int rb, u64*
     }
 }
 
-// ---- per-row rank-space fill + sort (replaces the global key sort) --------
+// ---- rank-space rows (replaces the global key sort) -------------------------
 // Row r = rank[v] of the rank-space CSR holds rank[w] for w in N(v), sorted.
-// Rows of <= 32 are sorted in registers (warp bitonic), rows of <= 128 in a
-// per-warp shared buffer, longer rows by one 256-thread CTA per row in
-// shared memory (<= kRowSortBlock; RMAT-22 rank rows 4.1 ms with rows up to
-// 1024 on the warps); graphs with longer rows take the global key sort.
-constexpr u32 kRowSortMid = 128;    // longer rows: one CTA per row
+// Short rows inside a slot tile are placed by counting (k_rank_fill_tiles),
+// rows up to 1024 slots sorted in a warp's registers (k_rank_fill_warp*),
+// longer ones by one 256-thread CTA per row in shared memory (<=
+// kRowSortBlock); graphs with longer rows take the global key sort. RMAT-22
+// (32 M slots): 4.1 ms with a warp walking 32 rows of up to 1024 slots, 2.2 ms
+// with rows > 128 on CTAs, 1.98 ms now (tiles 0.76, warps 0.44 + 0.24 + 0.38).
 constexpr u32 kRowSortBlock = 8192;
-constexpr int kFillWarps = 8;
-
-__device__ __forceinline__ u32 bitonic32(u32 x, u32 lane) {
-#pragma unroll
-    for (u32 k = 2; k <= 32; k <<= 1)
-#pragma unroll
-        for (u32 j = k >> 1; j > 0; j >>= 1) {
-            const u32 y = __shfl_xor_sync(G2M_FULL, x, j);
-            const bool up = (lane & k) == 0, lower = (lane & j) == 0;
-            x = (lower == up) ? min(x, y) : max(x, y);
-        }
-    return x;
-}
 
 // Bitonic sort of s[0, P) (P a power of two) by `nt` threads with index t;
 // sync() separates the stages.
@@ -1117,55 +1106,196 @@ __device__ __forceinline__ void bitonic_smem(u32* s, u32 P, u32 t, u32 nt, Sync&
         }
 }
 
-__global__ void __launch_bounds__(kFillWarps * 32)
-k_rank_fill(const u64* off, const u32* nbr, u64 nv, const u32* rank, const u64* rk_off, u32* rk_nbr, u32* hubs,
-            u32 mid) {
-    __shared__ u32 buf[kFillWarps][kRowSortMid];
-    const u32 lane = g2m_lane();
-    u32* sb = buf[threadIdx.x >> 5];
-    // rows in groups of 32: each lane fetches one row's offsets and its
-    // rank-space destination, so the per-row chain is nbr -> rank only
-    for (u64 v0 = ((blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5) * 32; v0 < nv;
-         v0 += (((u64)gridDim.x * blockDim.x) >> 5) * 32) {
-        const u64 vl = v0 + lane;
-        u64 bl = 0, dl = 0, ol = 0;
-        if (vl < nv) {
-            bl = off[vl];
-            dl = off[vl + 1] - bl;
-            if (dl) ol = rk_off[rank[vl]];
+// Rank-space rows by slot tiles: each CTA recovers its tile's rows (tile_rowmap),
+// gathers rank[nbr[s]] into shared memory, and places every slot of a row that
+// lies wholly inside the tile and has at most kTileRowMax slots at its rank
+// within the row (a count over the row in shared memory, no sort). The other
+// rows go on a list, pushed by the tile holding their first slot: rows of at
+// most kWarpRowMax slots to a warp each (k_rank_fill_warp), longer ones to a
+// CTA each (k_rank_fill_hubs).
+constexpr u32 kTileRowMax = 32;
+constexpr u32 kWarpRowMax = 256;
+__global__ void __launch_bounds__(kTileThreads)
+k_rank_fill_tiles(const u64* __restrict__ off, const u32* __restrict__ nbr, u64 nv, u64 slots,
+                  const u32* __restrict__ rank, const u64* __restrict__ rk_off, u32* __restrict__ rk_nbr) {
+    __shared__ u32 map[kTileSlots];
+    __shared__ u32 val[kTileSlots];
+    __shared__ u32 scr[kTileThreads / 32];
+    __shared__ u64 s_r[2];
+    constexpr u32 B = 4;   // slots per thread in flight
+    for (u64 tile = blockIdx.x; tile * kTileSlots < slots; tile += gridDim.x) {
+        const u64 S0 = tile * kTileSlots, S1 = min(S0 + kTileSlots, slots);
+        const u32 n = (u32)(S1 - S0);
+        tile_rowmap(off, nv, S0, S1, map, scr, s_r);
+        for (u32 p0 = threadIdx.x; p0 < n; p0 += B * kTileThreads) {
+            u32 x[B];
+#pragma unroll
+            for (u32 q = 0; q < B; ++q) {
+                const u32 p = p0 + q * kTileThreads;
+                x[q] = p < n ? __ldg(nbr + S0 + p) : 0u;
+            }
+#pragma unroll
+            for (u32 q = 0; q < B; ++q) {
+                const u32 p = p0 + q * kTileThreads;
+                if (p < n) val[p] = __ldg(rank + x[q]);
+            }
         }
-        const u32 nonempty = __ballot_sync(G2M_FULL, dl != 0);
-        for (u32 todo = nonempty; todo; todo &= todo - 1) {
-            const u32 j = __ffs(todo) - 1;
-            const u64 b = __shfl_sync(G2M_FULL, bl, j);
-            const u32 d = (u32)__shfl_sync(G2M_FULL, dl, j);
-            u32* out = rk_nbr + __shfl_sync(G2M_FULL, ol, j);
-            if (d > mid) {   // one CTA per row (k_rank_fill_hubs): no warp serialises them
-                if (lane == 0) push_hub(hubs, (u32)(v0 + j));
-                continue;
+        __syncthreads();
+        for (u32 p0 = threadIdx.x; p0 < n; p0 += B * kTileThreads) {
+            u32 u[B];
+            u64 b[B], e[B];
+#pragma unroll
+            for (u32 q = 0; q < B; ++q) {
+                const u32 p = p0 + q * kTileThreads;
+                u[q] = p < n ? map[p] : 0u;
+                b[q] = __ldg(off + u[q]);
+                e[q] = __ldg(off + u[q] + 1);
             }
-            if (d <= 32) {
-                u32 x = lane < d ? __ldg(rank + __ldg(nbr + b + lane)) : 0xffffffffu;
-                x = bitonic32(x, lane);
-                if (lane < d) out[lane] = x;
-                continue;
+            u64 dst[B];
+#pragma unroll
+            for (u32 q = 0; q < B; ++q) {
+                const u32 p = p0 + q * kTileThreads;
+                const bool in = p < n && b[q] >= S0 && e[q] <= S1 && e[q] - b[q] <= kTileRowMax;
+                dst[q] = in ? __ldg(rk_off + __ldg(rank + u[q])) : ~0ull;
             }
-            const u32 P = 1u << (32 - __clz(d - 1));
-            for (u32 i = lane; i < P; i += 32) sb[i] = i < d ? __ldg(rank + __ldg(nbr + b + i)) : 0xffffffffu;
-            __syncwarp();
-            bitonic_smem(sb, P, lane, 32, [] { __syncwarp(); });
-            for (u32 i = lane; i < d; i += 32) out[i] = sb[i];
-            __syncwarp();
+#pragma unroll
+            for (u32 q = 0; q < B; ++q) {
+                const u32 p = p0 + q * kTileThreads;
+                if (p >= n) continue;
+                if (dst[q] != ~0ull) {
+                    const u32 v = val[p], a = (u32)(b[q] - S0), L = (u32)(e[q] - b[q]);
+                    u32 c = 0;
+                    for (u32 t = 0; t < L; ++t) c += val[a + t] < v ? 1u : 0u;
+                    rk_nbr[dst[q] + c] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// The rows the tiles leave (longer than kTileRowMax, or across a tile edge):
+// rows of at most kWarpRowMax slots on one list, the rest on another
+// (warp-aggregated appends).
+__global__ void k_rank_classify(const u64* __restrict__ off, u64 nv, u32* __restrict__ wrows,
+                                u32* __restrict__ crows) {
+    const u32 lane = g2m_lane();
+    for (u64 v0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; v0 < nv;
+         v0 += (u64)gridDim.x * blockDim.x) {
+        const u64 v = v0 + lane;
+        u64 d = 0;
+        bool tile = true;
+        if (v < nv) {
+            const u64 b = off[v], e = off[v + 1];
+            d = e - b;
+            tile = d == 0 || (d <= kTileRowMax && b / kTileSlots == (e - 1) / kTileSlots);
+        }
+        const bool w = !tile && d <= kWarpRowMax, c = !tile && d > kWarpRowMax;
+        const u32 mw = __ballot_sync(G2M_FULL, w), mc = __ballot_sync(G2M_FULL, c);
+        u32 bw = 0, bc = 0;
+        if (lane == 0) {
+            if (mw) bw = atomicAdd(wrows, (u32)__popc(mw));
+            if (mc) bc = atomicAdd(crows, (u32)__popc(mc));
+        }
+        bw = __shfl_sync(G2M_FULL, bw, 0);
+        bc = __shfl_sync(G2M_FULL, bc, 0);
+        if (w) wrows[1 + bw + __popc(mw & g2m_lanemask_lt())] = (u32)v;
+        if (c) crows[1 + bc + __popc(mc & g2m_lanemask_lt())] = (u32)v;
+    }
+}
+
+// Bitonic sort of 32 * E values held E per lane (element lane * E + q in v[q]):
+// partners below E are in the same lane, the others one shuffle away.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(u32 (&v)[E], u32 lane) {
+    constexpr u32 P = 32u * E;
+#pragma unroll
+    for (u32 k = 2; k <= P; k <<= 1) {
+#pragma unroll
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            if (j >= (u32)E) {
+#pragma unroll
+                for (int q = 0; q < E; ++q) {
+                    const u32 i = lane * E + q;
+                    const u32 y = __shfl_xor_sync(G2M_FULL, v[q], j / E);
+                    const bool asc = (i & k) == 0, lower = (i & j) == 0;
+                    v[q] = (lower == asc) ? min(v[q], y) : max(v[q], y);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < E; ++q) {
+                    const int q2 = q ^ (int)j;
+                    if (q2 > q) {
+                        const bool asc = ((lane * E + q) & k) == 0;
+                        const u32 a = v[q], c = v[q2];
+                        const bool sw = asc ? (a > c) : (a < c);
+                        v[q] = sw ? c : a;
+                        v[q2] = sw ? a : c;
+                    }
+                }
+            }
         }
     }
 }
 
-// Rows longer than the warp threshold, one 256-thread CTA per row (several
-// CTAs per SM): the rows of a 32-row group no longer queue on one warp (the
-// long rows of a skewed graph sit together at the low original ids).
+template <int E>
+__device__ __forceinline__ void warp_row_sort(const u32* __restrict__ src, u32 d, const u32* __restrict__ rank,
+                                              u32* __restrict__ out, u32 lane) {
+    u32 x[E], v[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+        const u32 i = lane * E + q;
+        x[q] = i < d ? __ldg(src + i) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q) v[q] = lane * E + q < d ? __ldg(rank + x[q]) : 0xffffffffu;
+    warp_bitonic<E>(v, lane);
+#pragma unroll
+    for (int q = 0; q < E; ++q)
+        if (lane * E + q < d) out[lane * E + q] = v[q];
+}
+
+// Listed rows of at most kWarpRowMax slots, a warp each, sorted in registers.
+__global__ void __launch_bounds__(256)
+k_rank_fill_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ rank,
+                 const u64* __restrict__ rk_off, u32* __restrict__ rk_nbr, const u32* __restrict__ rows) {
+    const u32 lane = g2m_lane();
+    const u32 nr = rows[0];
+    for (u32 h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < nr; h += (gridDim.x * blockDim.x) >> 5) {
+        const u32 v = rows[1 + h];
+        const u64 b = __ldg(off + v);
+        const u32 d = (u32)(__ldg(off + v + 1) - b);
+        u32* out = rk_nbr + __ldg(rk_off + __ldg(rank + v));
+        const u32* src = nbr + b;
+        if (d <= 32) warp_row_sort<1>(src, d, rank, out, lane);
+        else if (d <= 64) warp_row_sort<2>(src, d, rank, out, lane);
+        else if (d <= 128) warp_row_sort<4>(src, d, rank, out, lane);
+        else warp_row_sort<8>(src, d, rank, out, lane);   // d <= kWarpRowMax
+    }
+}
+
+// Listed rows of 32 * E / 2 < d <= 32 * E, a warp each (the register file
+// holds the row: E = 16, 32).
+template <int E>
+__global__ void __launch_bounds__(128)
+k_rank_fill_warp_big(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ rank,
+                     const u64* __restrict__ rk_off, u32* __restrict__ rk_nbr, const u32* __restrict__ rows) {
+    const u32 lane = g2m_lane();
+    const u32 nr = rows[0];
+    for (u32 h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < nr; h += (gridDim.x * blockDim.x) >> 5) {
+        const u32 v = rows[1 + h];
+        const u64 b = __ldg(off + v);
+        const u32 d = (u32)(__ldg(off + v + 1) - b);
+        if (d <= 16u * E || d > 32u * E) continue;
+        warp_row_sort<E>(nbr + b, d, rank, rk_nbr + __ldg(rk_off + __ldg(rank + v)), lane);
+    }
+}
+
+// Listed rows longer than min_d, one 256-thread CTA per row (several CTAs per SM).
 constexpr int kRankFillThreads = 256;
 __global__ void __launch_bounds__(kRankFillThreads)
-k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_off, u32* rk_nbr, const u32* hubs) {
+k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_off, u32* rk_nbr, const u32* hubs,
+                 u32 min_d) {
     constexpr u32 kHubThreads = kRankFillThreads;
     __shared__ u32 sb[kRowSortBlock];
     const u32 nh = hubs[0];
@@ -1173,6 +1303,7 @@ k_rank_fill_hubs(const u64* off, const u32* nbr, const u32* rank, const u64* rk_
         const u32 v = hubs[1 + h];
         const u64 b = off[v];
         const u32 d = (u32)(off[v + 1] - b);   // <= kRowSortBlock (host check)
+        if (d <= min_d) continue;
         u32* out = rk_nbr + rk_off[rank[v]];
         const u32 P = 1u << (32 - __clz(d - 1));
         for (u32 i = threadIdx.x; i < P; i += kHubThreads) sb[i] = i < d ? __ldg(rank + __ldg(nbr + b + i)) : 0xffffffffu;
@@ -1266,15 +1397,31 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
     // (a slot-parallel gather into the rank-space rows + cub::DeviceSegmentedSort
     // measured 0.5 + 8.3 ms on RMAT-22 against 2.2 ms for the per-row fill below)
     if (nv && slots && g->maxdeg <= kRowSortBlock && !getenv("G2M_RANK_RADIX")) {
-        u32* hubs = nullptr;
-        const u32 mid = getenv("G2M_RANK_MID") ? (u32)atoi(getenv("G2M_RANK_MID")) : kRowSortMid;
-        G2M_TRY(hub_list(st, slots, std::min(mid, kRowSortMid), &hubs));
-        st->launches += 2;
-        k_rank_fill<<<grid_for(st, nv * 32, kFillWarps * 32), kFillWarps * 32, 0, st->stream>>>(
-            g->off.as<u64>(), g->nbr.as<u32>(), nv, rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs,
-            std::min(mid, kRowSortMid));
-        k_rank_fill_hubs<<<st->sms * 6, kRankFillThreads, 0, st->stream>>>(
-            g->off.as<u64>(), g->nbr.as<u32>(), rank.as<u32>(), g->rk_off.as<u64>(), g->rk_nbr.as<u32>(), hubs);
+        const u64 tiles = (slots + kTileSlots - 1) / kTileSlots;
+        // lists: [0] = count, then rows; at most one row per tile crosses its edge
+        G2M_TRY(st->hubs.ensure((slots / (kTileRowMax + 1) + tiles + 2) * 4));
+        G2M_TRY(st->mids.ensure((slots / (kWarpRowMax + 1) + tiles + 2) * 4));
+        u32* wrows = st->hubs.as<u32>();
+        u32* crows = st->mids.as<u32>();
+        G2M_CUDA(cudaMemsetAsync(wrows, 0, 4, st->stream));
+        G2M_CUDA(cudaMemsetAsync(crows, 0, 4, st->stream));
+        ++st->launches;
+        k_rank_classify<<<grid_for(st, nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), nv, wrows, crows);
+        G2M_CUDA(cudaGetLastError());
+        // disjoint rows; on five side streams they ran no faster (2.08 vs 1.98 ms
+        // RMAT-22: the tile pass fills every SM first)
+        const u64* o = g->off.as<u64>();
+        const u32* nb = g->nbr.as<u32>();
+        const u32* rk = rank.as<u32>();
+        const u64* ro = g->rk_off.as<u64>();
+        u32* rn = g->rk_nbr.as<u32>();
+        st->launches += 5;
+        k_rank_fill_tiles<<<(int)std::min<u64>(tiles, (u64)st->sms * 7), kTileThreads, 0, st->stream>>>(
+            o, nb, nv, slots, rk, ro, rn);
+        k_rank_fill_warp<<<st->sms * 8, 256, 0, st->stream>>>(o, nb, rk, ro, rn, wrows);
+        k_rank_fill_warp_big<16><<<st->sms * 4, 128, 0, st->stream>>>(o, nb, rk, ro, rn, crows);
+        k_rank_fill_warp_big<32><<<st->sms * 4, 128, 0, st->stream>>>(o, nb, rk, ro, rn, crows);
+        k_rank_fill_hubs<<<st->sms * 6, kRankFillThreads, 0, st->stream>>>(o, nb, rk, ro, rn, crows, 1024u);
         G2M_CUDA(cudaGetLastError());
     } else if (nv && slots) {
         int rb = 1;
