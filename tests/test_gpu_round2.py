@@ -335,3 +335,59 @@ def test_cycle4_coarse_staging_rounds(monkeypatch, rounds):
     monkeypatch.setenv("G2M_C4_ROUNDS", rounds)
     g2 = GR.from_edges(G.rmat_edges(14, 16, 8), num_vertices=1 << 14)
     assert EX.execute(g2, f, EX._default_tasks(g2, f))[0] == want
+
+
+def _rank_host(g, sym_deg):
+    """Host restatement of the rank relabelling: rank = position in the
+    (degree, id) order; row rank[v] = sorted rank[w], w in N(v)."""
+    n = g.num_vertices
+    off = np.asarray(g.row_offsets, dtype=np.int64)
+    order = np.lexsort((np.arange(n), sym_deg))
+    rank = np.empty(n, dtype=np.int64)
+    rank[order] = np.arange(n)
+    deg = np.diff(off)
+    roff = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(deg[order], out=roff[1:])
+    rnbr = np.empty(int(off[-1]), dtype=np.int64)
+    for v in range(n):
+        r = rank[v]
+        rnbr[roff[r]:roff[r + 1]] = np.sort(rank[g.neighbors[off[v]:off[v + 1]].astype(np.int64)])
+    return roff, rnbr
+
+
+def _row_class_graph():
+    """Rows of every length class of the rank build (in-tile rows <= 32 slots,
+    rows across 4096-slot tile edges, warp register sorts up to 256 / 512 /
+    1024, CTA sorts beyond), runs of isolated vertices inside tiles, and a
+    slot count that is not a multiple of 32."""
+    n = 9000
+    rng = np.random.default_rng(17)
+    e = [np.column_stack([rng.integers(0, n, 30001), rng.integers(0, n, 30001)])]
+    for hub, k in ((100, 33), (200, 200), (300, 300), (400, 700), (500, 1100), (600, 2500), (700, 31)):
+        nb = rng.choice(np.arange(4000, n), size=k, replace=False)
+        e.append(np.column_stack([np.full(k, hub), nb]))
+    ed = np.concatenate(e)
+    ed = ed[(ed[:, 0] != ed[:, 1]) & ((ed[:, 0] < 1500) | (ed[:, 0] >= 2500)) & ((ed[:, 1] < 1500) | (ed[:, 1] >= 2500))]
+    return GR.from_edges(ed, num_vertices=n)     # ids 1500..2499 isolated
+
+
+def test_rank_copy_equals_host_restatement():
+    g = _row_class_graph()
+    assert g.max_degree > 1024 and int(np.asarray(g.row_offsets)[-1]) % 32 != 0
+    sym_deg = np.diff(np.asarray(g.row_offsets, dtype=np.int64))
+    for gg in (g, pm.orient(g)):   # symmetric rows, then the oriented DAG (degrees of g)
+        roff, rnbr = _rank_host(gg, sym_deg)
+        rg = GR.rank_relabel(gg)
+        assert np.array_equal(np.asarray(rg.row_offsets, dtype=np.int64), roff)
+        assert np.array_equal(rg.neighbors.astype(np.int64), rnbr)
+
+
+def test_device_orientation_tiles_equal_host():
+    """The slot-tile orientation on graphs whose rows span many tiles, whose
+    tiles hold long runs of empty rows, and whose slot count is a tile
+    multiple or not."""
+    for g in (_row_class_graph(), GR.from_edges(np.column_stack([np.zeros(5000, np.int64),
+                                                                 np.arange(1, 5001)]), num_vertices=20000)):
+        og = pm.orient(g)
+        ho = orient_host(g)
+        assert og == ho and og.oriented
