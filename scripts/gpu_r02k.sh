@@ -13,4 +13,3 @@ run c4 --workload c4 --steps 3 --warmup 3
 run diamond --workload diamond --steps 3 --warmup 3
 run mc3 --workload mc3
 run mc4 --workload mc4 --steps 3 --warmup 3
-timeout 700 compute-sanitizer --tool racecheck --print-limit 20 python scripts/sanitize_workload.py 10 > gpurun_out/${T}_sanitize_racecheck.log 2>&1; echo racecheck rc=$?; grep -E "SUMMARY|MISMATCHES" gpurun_out/${T}_sanitize_racecheck.log | head -3
