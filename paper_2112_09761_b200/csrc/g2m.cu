@@ -2556,44 +2556,6 @@ extern "C" int g2m_clique_count(const g2m_graph* g, int32_t k, const g2m_task_sp
     return clique_impl(g, k, part, fallback, cfg, counts, stats, st);
 }
 
-// Heaviest sources first inside each CTA tier's list (longest processing
-// time first): a tier's CTAs take sources from one atomic queue, so a heavy
-// source grabbed last sets the tier's tail. Key = out-degree, descending.
-__global__ void k_list_degs(const u64* off, const u32* list, u64 n, u32* keys) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        const u32 v = list[i];
-        keys[i] = (u32)(off[v + 1] - off[v]);
-    }
-}
-
-static int lpt_order(DevState* st, const u64* off, u32* lists, u64 stride, const uint64_t* sizes,
-                     std::initializer_list<int> classes, int dbits) {
-    u64 nmax = 0;
-    for (int c : classes) nmax = std::max<u64>(nmax, sizes[c]);
-    if (nmax < 2) return G2M_OK;
-    G2M_TRY(st->tmp2.ensure(nmax * 8));
-    G2M_TRY(st->tmp3.ensure(nmax * 4));
-    u32* kin = st->tmp2.as<u32>();
-    u32* kout = kin + nmax;
-    u32* vout = st->tmp3.as<u32>();
-    for (int c : classes) {
-        const u64 n = sizes[c];
-        if (n < 2) continue;
-        u32* list = lists + (u64)c * stride;
-        ++st->launches;
-        k_list_degs<<<grid_for(st, n, 256), 256, 0, st->stream>>>(off, list, n, kin);
-        G2M_CUDA(cudaGetLastError());
-        size_t tb = 0;
-        G2M_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, kin, kout, list, vout, (int64_t)n, 0, dbits,
-                                                           st->stream));
-        G2M_TRY(st->cub_tmp.ensure(tb));
-        G2M_CUDA(cub::DeviceRadixSort::SortPairsDescending(st->cub_tmp.p, tb, kin, kout, list, vout, (int64_t)n, 0,
-                                                           dbits, st->stream));
-        G2M_CUDA(cudaMemcpyAsync(list, vout, n * 4, cudaMemcpyDeviceToDevice, st->stream));
-    }
-    return G2M_OK;
-}
-
 // g2m_clique_count with the device lock held
 static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part, const g2m_kernel* fallback,
                        const g2m_run_config* cfg, uint64_t* counts, g2m_run_stats* stats, DevState* st) {
@@ -2647,8 +2609,6 @@ static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
     G2M_CUDA(cudaMemcpyAsync(spans, dspans, kClasses * 4, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
     const u32* lists = st->tasks_b.as<u32>();
-    if (getenv("G2M_CLIQUE_LPT") && atoi(getenv("G2M_CLIQUE_LPT")))
-        G2M_TRY(lpt_order(st, off, st->tasks_b.as<u32>(), stride, sizes, {2, 3, 4, 5, 7}, 13));
     if (getenv("G2M_DEBUG"))
         fprintf(stderr, "[g2m] clique k=%d buckets: pairs %llu warp<=64:%llu 128:%llu 256:%llu 512:%llu 1024:%llu 4096:%llu generic:%llu\n",
                 k, (unsigned long long)sizes[8], (unsigned long long)sizes[1], (unsigned long long)sizes[2], (unsigned long long)sizes[3],
