@@ -2579,7 +2579,13 @@ static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
     const u64* wpre = nullptr;
     u64 wchunk = 0;
     G2M_TRY(source_weights(g, st, part, 0, k, &wpre, &wchunk));
+    const bool dbgc = getenv("G2M_DEBUG") != nullptr;
+    auto tc0 = Clock::now();
     const g2m_clique::HubCore core = ensure_core(g, st);
+    if (dbgc) {
+        cudaStreamSynchronize(st->stream);
+        fprintf(stderr, "[g2m] hub core: %.2f ms (setup since call start %.2f ms)\n", ms_since(tc0), ms_since(t0));
+    }
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
     // counters: ctr[8..9] count (lo, hi), ctr[10..] one work counter per launch
     G2M_TRY(st->counters.ensure(32 * 8));

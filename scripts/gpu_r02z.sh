@@ -1,7 +1,5 @@
-# round 2 (z): k = 5 heavy rows counted word-outer (G2M_CL5_Q=1) vs lane-per-l (0); e2e phases of diamond after the max-degree fix
 mkdir -p gpurun_out
-timeout 900 python scripts/ab_env.py 22 cl5 "G2M_CL5_Q=0|G2M_CL5_Q=1" debug > gpurun_out/z_cl5_q_ab.txt 2>&1; echo ab rc=$?
-grep -v "^\[g2m\]   launch" gpurun_out/z_cl5_q_ab.txt | grep -v "class" | tail -12
-grep "launch 1:" gpurun_out/z_cl5_q_ab.txt
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
-timeout 600 python scripts/e2e_profile.py diamond > gpurun_out/z_prof_diamond.txt 2>&1; grep "api ms" gpurun_out/z_prof_diamond.txt
+python scripts/e2e_breakdown.py cl4 > gpurun_out/z_e2e_breakdown_cl4.txt 2>&1
+G2M_DEBUG=1 python scripts/e2e_debug.py cl4 > gpurun_out/z_e2e_debug_cl4b.txt 2>&1
+python scripts/e2e_breakdown.py tc > gpurun_out/z_e2e_breakdown_tc.txt 2>&1
+cat gpurun_out/z_e2e_breakdown_cl4.txt gpurun_out/z_e2e_breakdown_tc.txt; grep -v "launch\|class" gpurun_out/z_e2e_debug_cl4b.txt | tail -14
