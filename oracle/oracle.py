@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-LIB = HERE / "_ref" / "liboracle.so"
+LIB = HERE / "_build" / "liboracle.so"
 
 MAXL, MAXP, MAXC = 9, 32, 24
 _ACT = {"descend": 0, "emit_count": 1, "binomial_count": 2, "emit_match": 3}
@@ -35,7 +35,7 @@ _lib = None
 
 
 def build() -> Path:
-    """Compile oracle.c into oracle/_ref/liboracle.so (gcc)."""
+    """Compile oracle.c into oracle/_build/liboracle.so (gcc)."""
     subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     return LIB
 
