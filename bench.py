@@ -303,7 +303,7 @@ def kernel_operands(family: str, gd, forest, tasks, local, rank, args):
                               "offsets + the wedge ends N(v) & [lo_x, r) (4 B each), plus one 4 B "
                               "counter read-modify-write per wedge (8 B)"), \
             {"wedges": wedges, "sources": src}
-    if family == "diamond":
+    if family in ("diamond", "diamond-allreduce"):
         og = GR.orient(gd, device=local)
         ob, probes, _, src = og.device_graph(local).kernel_work(2)     # support tiers: no hub core
         # + one support counter RMW per triangle edge (3 per triangle found) and
@@ -480,15 +480,26 @@ def main():
     # ------------------------------------------------------------------ b200
     rr = D.shard(rank, world, device=local)
     family = EX.kernel_family(gd, forest, tasks, rr=rr)
+    # diamonds on N > 1 GPUs: the support kernels on each rank's sources, one
+    # all-reduce of the support array, C(t, 2) over each rank's slot share
+    support_ar = world > 1 and EX._is_diamond_count(gd, forest, tasks, None, None, None)
+    if support_ar:
+        family = "diamond-allreduce"
     if world > 1:
         config["parallelism"] = (
             f"{world} GPU(s): graph replicated, edge tasks by chunked round-robin (c = 2 x resident warps), "
             f"LGS/wedge sources by the workload estimator "
-            f"({EX.SOURCE_SPLIT}:{EX.SOURCE_CHUNK.get(family, '-')})")
+            f"({EX.SOURCE_SPLIT}:{EX.SOURCE_CHUNK.get(family, '-')})"
+            + ("; diamond support summed by one all-reduce of the per-edge support array" if support_ar else ""))
+
+    def run_share(gg, ff, tt):
+        if support_ar:
+            return D.diamond_count(gg, rank, world, device=local, rr=rr, name=ff.single().pattern.name)
+        counts, st, _, _ = EX.execute(gg, ff, tt, device=local, rr=rr, search="auto")
+        return counts, st
 
     def step():   # run_job's search choice (DFS / bounded-frontier BFS), logged as "bounded-bfs"
-        counts, st, _, _ = EX.execute(gd, forest, tasks, device=local, rr=rr, search="auto")
-        return counts, st
+        return run_share(gd, forest, tasks)
 
     for _ in range(args.warmup):
         counts, st = step()
@@ -551,7 +562,7 @@ def main():
                 api_call(args.workload, hg)
             else:
                 pr = prepare(args.workload, hg)
-                EX.execute(pr.graph, pr.forest, pr.tasks, device=local, rr=rr, search="auto")
+                run_share(pr.graph, pr.forest, pr.tasks)
             dt = time.perf_counter() - t1
             del hg
             # the previous call's graphs (and their device replicas) go before the
@@ -620,6 +631,8 @@ def main():
                 "kernel": {"lgs": "bitmap local-graph clique tiers (concurrent streams)",
                            "cycle4": "4-cycle wedge-aggregation tiers",
                            "diamond": "edge triangle-support tiers + sum C(t,2)",
+                           "diamond-allreduce": "edge triangle-support tiers on each rank's sources, "
+                                                "all-reduce of the support array, sum C(t,2) per slot share",
                            "plan": "generated plan kernel (DFS or bounded BFS)"}[family],
                 "kernel_ms_per_step": kms,
                 "kernel_share": kms / ms if ms else None,

@@ -58,7 +58,7 @@
 extern "C" {
 #endif
 
-#define G2M_ABI_VERSION 6
+#define G2M_ABI_VERSION 7
 
 #define G2M_OK 0
 #define G2M_EUSAGE 1
@@ -299,6 +299,22 @@ int g2m_cycle4_count(const g2m_graph* g, const g2m_task_spec* part, const g2m_ru
  * over task partitions). counts_lo_hi receives (lo, hi). */
 int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, uint64_t* counts_lo_hi,
                       g2m_run_stats* stats);
+
+/* The two halves of g2m_diamond_count for a multi-GPU run, where per-edge
+ * support is NOT additive over a source split but IS additive as an array:
+ * g2m_diamond_support adds into `tsup` (device memory of g's device,
+ * *num_slots u32, zeroed by the caller) the support contributions of the
+ * triangles whose DAG source is in `part` (chunked round-robin share, as for
+ * g2m_clique_count; null = all). With tsup == NULL it only builds the
+ * oriented rank-space copy and reports *num_slots. After an all-reduce (sum)
+ * of tsup over the ranks, g2m_support_choose2 gives Σ C(tsup[s], 2) over a
+ * slot share [lo, hi), additive over the ranks' shares. Replaces the
+ * edge-parallel plan kernel of run_on_devices for the diamond plan
+ * (scheduler.py:207-239, plan.py:177-198). */
+int g2m_diamond_support(const g2m_graph* g, const g2m_task_spec* part, uint32_t* tsup,
+                        uint64_t* num_slots, g2m_run_stats* stats);
+int g2m_support_choose2(const g2m_graph* g, const uint32_t* tsup, uint64_t lo, uint64_t hi,
+                        uint64_t* counts_lo_hi, g2m_run_stats* stats);
 
 /* Batched sorted-set kernels (setops.py:35-84). Lists are concatenated u32
  * arrays addressed by u64 offsets; op: 0 intersect, 1 intersect_count,

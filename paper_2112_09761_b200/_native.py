@@ -17,7 +17,7 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libg2m.so"
 DEVICE_HEADER = PKG_DIR / "csrc" / "g2m_device.cuh"
 
-ABI_VERSION = 6                     # G2M_ABI_VERSION in include/g2m.h
+ABI_VERSION = 7                     # G2M_ABI_VERSION in include/g2m.h
 G2M_OK, G2M_EUSAGE, G2M_EBUDGET, G2M_ECUDA, G2M_STOPPED = 0, 1, 2, 3, 4
 TASKS_EDGE, TASKS_VERTEX = 0, 1
 SRC_IMPLICIT, SRC_PAIRS, SRC_VERTICES, SRC_INDEX = 0, 1, 2, 3
@@ -120,6 +120,9 @@ SIGNATURES = {
     "g2m_cycle4_count": (C.c_int, [_P, C.POINTER(TaskSpec), C.POINTER(RunConfig), _u64p,
                                    C.POINTER(RunStats)]),
     "g2m_diamond_count": (C.c_int, [_P, C.POINTER(RunConfig), _u64p, C.POINTER(RunStats)]),
+    "g2m_diamond_support": (C.c_int, [_P, C.POINTER(TaskSpec), C.c_void_p, _u64p, C.POINTER(RunStats)]),
+    "g2m_support_choose2": (C.c_int, [_P, C.c_void_p, C.c_uint64, C.c_uint64, _u64p,
+                                      C.POINTER(RunStats)]),
     "g2m_setop_batch": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, _u32p, _u64p, _u32p,
                                   _u64p, _i64p, _u64p, _u32p]),
 }

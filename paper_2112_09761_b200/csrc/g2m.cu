@@ -2693,6 +2693,83 @@ static int clique_impl(const g2m_graph* g, int32_t k, const g2m_task_spec* part,
 // triangles on the edge, accumulated by the bitmap triangle kernels over the
 // rank-space DAG of the degree orientation (one support counter per DAG edge).
 
+// Triangle support of every edge of the degree-oriented rank-space DAG of a
+// symmetric graph, from the triangles whose DAG source is in `part` (all when
+// null), added into tsup (og->slots u32 per rank-space slot). Builds the
+// oriented copy and its rank relabelling once per graph. Device lock held.
+static int diamond_support_impl(const g2m_graph* g, const g2m_task_spec* part, u32* tsup, g2m_run_stats* S,
+                                DevState* st, const g2m_graph** og_out) {
+    g2m_graph* gm = const_cast<g2m_graph*>(g);
+    {
+        std::lock_guard<std::mutex> glk(gm->mu);
+        if (!gm->oriented_copy) {
+            g2m_graph* o = nullptr;
+            G2M_TRY(orient_impl(g, st, &o));
+            gm->oriented_copy.reset(o);
+        }
+    }
+    const g2m_graph* og = gm->oriented_copy.get();
+    *og_out = og;
+    G2M_TRY(ensure_rank(og, st));
+    if (!tsup) return G2M_OK;
+    u64 rr_chunk = 0;
+    u32 parts = 1, pt = 0;
+    if (part && part->rr_chunk) {
+        if (part->rr_parts == 0) return fail(G2M_EUSAGE, "rr_parts must be positive");
+        rr_chunk = part->rr_chunk;
+        parts = part->rr_parts;
+        pt = part->rr_part;
+    }
+    const u64* off = og->rk_off.as<u64>();
+    const u32* nbr = og->rk_nbr.as<u32>();
+    const u64* wpre = nullptr;
+    u64 wchunk = 0;
+    G2M_TRY(source_weights(og, st, part, 0, 3, &wpre, &wchunk));
+    G2M_TRY(st->counters.ensure(32 * 8));
+    u64* ctr = st->counters.as<u64>();
+    G2M_CUDA(cudaMemsetAsync(ctr, 0, 32 * 8, st->stream));
+    const u64 stride = std::max<u64>(og->nv, 1);
+    G2M_TRY(st->tasks_b.ensure((u64)kClasses * stride * 4));
+    G2M_TRY(st->tasks_a.ensure(kClasses * 8 + kClasses * 4));
+    u64* dsizes = st->tasks_a.as<u64>();
+    u32* dspans = (u32*)(dsizes + kClasses);
+    G2M_CUDA(cudaMemsetAsync(dsizes, 0, kClasses * 12, st->stream));
+    if (og->nv) {
+        ++st->launches;
+        g2m_clique::k_clique_bucket<<<grid_for(st, og->nv, 256), 256, 0, st->stream>>>(
+            off, nbr, og->nv, 2, 4096, 0, rr_chunk, parts, pt, wpre, wchunk, st->tasks_b.as<u32>(), stride, dsizes,
+            dspans);
+        G2M_CUDA(cudaGetLastError());
+    }
+    uint64_t sizes[kClasses];
+    uint32_t spans[kClasses];
+    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, kClasses * 8, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaMemcpyAsync(spans, dspans, kClasses * 4, cudaMemcpyDeviceToHost, st->stream));
+    G2M_CUDA(cudaStreamSynchronize(st->stream));
+    if (sizes[6]) return fail(G2M_EUSAGE, "diamond support kernels cover out-degrees <= 4096");
+    G2M_TRY((clique_launch_all<3, true>(off, nbr, st, st->tasks_b.as<u32>(), stride, sizes, spans, ctr + 8,
+                                         &S->kernel_ms, tsup)));
+    S->tasks = 0;
+    for (int c = 1; c < kClasses; ++c) S->tasks += sizes[c];
+    return G2M_OK;
+}
+
+// Σ C(tsup[s], 2) over slots [lo, hi) into ctr (lo, hi), timed into kms.
+static int support_choose2(DevState* st, const u32* tsup, u64 lo, u64 hi, u64* ctr, double* kms) {
+    G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
+    if (hi > lo) {
+        ++st->launches;
+        g2m_clique::k_sum_choose2<<<grid_for(st, hi - lo, 256), 256, 0, st->stream>>>(tsup + lo, hi - lo, ctr);
+        G2M_CUDA(cudaGetLastError());
+    }
+    G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
+    G2M_CUDA(cudaEventSynchronize(st->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, st->ev0, st->ev1);
+    *kms += ms;
+    return G2M_OK;
+}
+
 extern "C" int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, uint64_t* counts,
                                  g2m_run_stats* stats) {
     (void)cfg;
@@ -2707,71 +2784,78 @@ extern "C" int g2m_diamond_count(const g2m_graph* g, const g2m_run_config* cfg, 
     g2m_run_stats* S = stats ? stats : &local;
     std::memset(S, 0, sizeof(*S));
     const uint64_t l0 = st->launches;
-    g2m_graph* gm = const_cast<g2m_graph*>(g);
-    {
-        std::lock_guard<std::mutex> glk(gm->mu);
-        if (!gm->oriented_copy) {
-            g2m_graph* o = nullptr;
-            G2M_TRY(orient_impl(g, st, &o));
-            gm->oriented_copy.reset(o);
-        }
-    }
-    const g2m_graph* og = gm->oriented_copy.get();
-    G2M_TRY(ensure_rank(og, st));
-    const u64* off = og->rk_off.as<u64>();
-    const u32* nbr = og->rk_nbr.as<u32>();
+    const g2m_graph* og = nullptr;
+    G2M_TRY(diamond_support_impl(g, nullptr, nullptr, S, st, &og));   // oriented copy + rank (untimed)
     G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
-    G2M_TRY(st->counters.ensure(32 * 8));
-    u64* ctr = st->counters.as<u64>();
-    G2M_CUDA(cudaMemsetAsync(ctr, 0, 32 * 8, st->stream));
     DevBuf& tsup = st->tmp1;   // grow-only scratch (the rank build that also uses it is done)
     G2M_TRY(tsup.ensure(std::max<u64>(og->slots, 1) * 4));
     G2M_CUDA(cudaMemsetAsync(tsup.p, 0, std::max<u64>(og->slots, 1) * 4, st->stream));
-    const u64 stride = std::max<u64>(og->nv, 1);
-    G2M_TRY(st->tasks_b.ensure((u64)kClasses * stride * 4));
-    G2M_TRY(st->tasks_a.ensure(kClasses * 8 + kClasses * 4));
-    u64* dsizes = st->tasks_a.as<u64>();
-    u32* dspans = (u32*)(dsizes + kClasses);
-    G2M_CUDA(cudaMemsetAsync(dsizes, 0, kClasses * 12, st->stream));
-    if (og->nv) {
-        ++st->launches;
-        g2m_clique::k_clique_bucket<<<grid_for(st, og->nv, 256), 256, 0, st->stream>>>(
-            off, nbr, og->nv, 2, 4096, 0, 0, 1, 0, nullptr, 0, st->tasks_b.as<u32>(), stride, dsizes, dspans);
-        G2M_CUDA(cudaGetLastError());
-    }
-    uint64_t sizes[kClasses];
-    uint32_t spans[kClasses];
-    G2M_CUDA(cudaMemcpyAsync(sizes, dsizes, kClasses * 8, cudaMemcpyDeviceToHost, st->stream));
-    G2M_CUDA(cudaMemcpyAsync(spans, dspans, kClasses * 4, cudaMemcpyDeviceToHost, st->stream));
-    G2M_CUDA(cudaStreamSynchronize(st->stream));
-    if (sizes[6]) return fail(G2M_EUSAGE, "diamond support kernels cover out-degrees <= 4096");
-    G2M_TRY((clique_launch_all<3, true>(off, nbr, st, st->tasks_b.as<u32>(), stride, sizes, spans, ctr + 8,
-                                         &S->kernel_ms, tsup.as<u32>())));
-    {
-        G2M_CUDA(cudaEventRecord(st->ev0, st->stream));
-        ++st->launches;
-        g2m_clique::k_sum_choose2<<<grid_for(st, og->slots, 256), 256, 0, st->stream>>>(tsup.as<u32>(), og->slots,
-                                                                                           ctr + 16);
-        G2M_CUDA(cudaGetLastError());
-        G2M_CUDA(cudaEventRecord(st->ev1, st->stream));
-        G2M_CUDA(cudaEventSynchronize(st->ev1));
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, st->ev0, st->ev1);
-        S->kernel_ms += ms;
-    }
+    G2M_TRY(diamond_support_impl(g, nullptr, tsup.as<u32>(), S, st, &og));
+    u64* ctr = st->counters.as<u64>();
+    G2M_TRY(support_choose2(st, tsup.as<u32>(), 0, og->slots, ctr + 16, &S->kernel_ms));
     uint64_t h[2] = {0, 0};
     G2M_CUDA(cudaMemcpyAsync(h, ctr + 16, 16, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
     G2M_CUDA(cudaEventSynchronize(st->evs1));
     counts[0] = h[0];
     counts[1] = h[1];
-    S->tasks = 0;
-    for (int c = 1; c < kClasses; ++c) S->tasks += sizes[c];
     float dm = 0.f;
     cudaEventElapsedTime(&dm, st->evs0, st->evs1);
     S->device_ms = dm;
     S->launches = st->launches - l0;
     S->total_ms = ms_since(t0);
+    return G2M_OK;
+}
+
+extern "C" int g2m_diamond_support(const g2m_graph* g, const g2m_task_spec* part, uint32_t* tsup,
+                                   uint64_t* num_slots, g2m_run_stats* stats) {
+    if (!g || !num_slots) return fail(G2M_EUSAGE, "null argument");
+    if (g->oriented) return fail(G2M_EUSAGE, "diamond support needs the symmetric graph");
+    auto t0 = Clock::now();
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    g2m_run_stats local{};
+    g2m_run_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    const uint64_t l0 = st->launches;
+    const g2m_graph* og = nullptr;
+    G2M_TRY(diamond_support_impl(g, part, nullptr, S, st, &og));
+    *num_slots = og->slots;
+    if (tsup) {
+        G2M_CUDA(cudaEventRecord(st->evs0, st->stream));
+        G2M_TRY(diamond_support_impl(g, part, tsup, S, st, &og));
+        G2M_CUDA(cudaEventRecord(st->evs1, st->stream));
+        G2M_CUDA(cudaEventSynchronize(st->evs1));
+        float dm = 0.f;
+        cudaEventElapsedTime(&dm, st->evs0, st->evs1);
+        S->device_ms = dm;
+    }
+    S->launches = st->launches - l0;
+    S->total_ms = ms_since(t0);
+    return G2M_OK;
+}
+
+extern "C" int g2m_support_choose2(const g2m_graph* g, const uint32_t* tsup, uint64_t lo, uint64_t hi,
+                                   uint64_t* counts, g2m_run_stats* stats) {
+    if (!g || !tsup || !counts) return fail(G2M_EUSAGE, "null argument");
+    if (lo > hi) return fail(G2M_EUSAGE, "lo > hi");
+    DevState* st;
+    G2M_TRY(dev_state(g->dev, &st));
+    std::lock_guard<std::mutex> lk(st->mu);
+    G2M_CUDA(cudaSetDevice(g->dev));
+    const g2m_graph* og = g->oriented ? g : const_cast<g2m_graph*>(g)->oriented_copy.get();
+    if (!og || hi > og->slots) return fail(G2M_EUSAGE, "slot range beyond the support array");
+    g2m_run_stats local{};
+    g2m_run_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    G2M_TRY(st->counters.ensure(32 * 8));
+    u64* ctr = st->counters.as<u64>();
+    G2M_CUDA(cudaMemsetAsync(ctr + 16, 0, 16, st->stream));
+    G2M_TRY(support_choose2(st, tsup, lo, hi, ctr + 16, &S->kernel_ms));
+    G2M_CUDA(cudaMemcpy(counts, ctr + 16, 16, cudaMemcpyDeviceToHost));
+    S->device_ms = S->kernel_ms;
     return G2M_OK;
 }
 

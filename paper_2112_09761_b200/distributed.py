@@ -9,8 +9,15 @@ so they travel as four 32-bit limbs in int64 lanes: a sum over any
 realistic number of ranks cannot overflow a lane, and carries are resolved
 after the reduction.
 
+The one path with a real exchange step is the diamond count on the support
+kernels: per-edge triangle support is not additive over a source split (the
+count is Σ_e C(t_e, 2)), but the support ARRAY is. Each rank adds its
+sources' triangles into a device array, one all-reduce (sum) of that array
+(4 B per DAG edge: 1 GB at RMAT-24) completes every edge's support, and each
+rank sums C(t_e, 2) over its own slot share (``diamond_count``).
+
 ``torch.distributed`` is the transport (NCCL on GPUs, gloo on CPU for the
-tests); nothing here touches the kernels.
+tests).
 """
 from __future__ import annotations
 
@@ -73,3 +80,56 @@ def allreduce_max(x: float, group=None, device=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+class SupportStats:
+    """device_ms / kernel_ms / tasks / launches of one distributed diamond step."""
+
+    def __init__(self, device_ms: float, kernel_ms: float, tasks: int, launches: int):
+        self.device_ms, self.kernel_ms, self.tasks, self.launches = device_ms, kernel_ms, tasks, launches
+
+
+def diamond_count(g, rank: int, world: int, device: int = 0, rr=None, group=None,
+                  name: str = "diamond"):
+    """Diamond count of the symmetric graph g over ``world`` ranks: support
+    of the rank's sources (``rr``, the chunked round-robin / estimator share
+    of executor.source_spec) into a device array, all-reduce (sum), then
+    Σ C(t, 2) over the rank's slot share. Returns this rank's additive share
+    of the count ({name: share}; ``allreduce_counts`` gives the total) and
+    the step's stats (device time = support + all-reduce + sum, CUDA events
+    on the rank's device)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from . import _native as N
+    from . import executor as EX
+
+    dg = g.device_graph(device)
+    n = C.c_uint64(0)
+    N.check(N.lib().g2m_diamond_support(dg.handle, None, None, C.byref(n), None), "diamond support")
+    slots = int(n.value)
+    dev = torch.device("cuda", device)
+    tsup = torch.zeros(max(slots, 1), dtype=torch.int32, device=dev)
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(torch.cuda.current_stream(dev))
+    spec = EX.source_spec(rr, family="lgs")
+    st = N.RunStats()
+    N.check(N.lib().g2m_diamond_support(dg.handle, C.byref(spec), C.c_void_p(tsup.data_ptr()), C.byref(n),
+                                        C.byref(st)), "diamond support")
+    if world > 1:   # the support kernels' stream is drained when the call returns
+        import torch.distributed as dist
+        dist.all_reduce(tsup, op=dist.ReduceOp.SUM, group=group)
+    torch.cuda.synchronize(dev)
+    lo, hi = rank * slots // world, (rank + 1) * slots // world
+    words = np.zeros(2, dtype=np.uint64)
+    st2 = N.RunStats()
+    N.check(N.lib().g2m_support_choose2(dg.handle, C.c_void_p(tsup.data_ptr()), lo, hi,
+                                        N.ptr(words, C.c_uint64), C.byref(st2)), "support choose2")
+    ev1.record(torch.cuda.current_stream(dev))
+    ev1.synchronize()
+    share = int(words[0]) | (int(words[1]) << 64)
+    return {name: share}, SupportStats(ev0.elapsed_time(ev1), st.kernel_ms + st2.kernel_ms,
+                                       int(st.tasks), int(st.launches) + 1)

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-python scripts/e2e_breakdown.py cl4 > gpurun_out/z_e2e_breakdown_cl4.txt 2>&1
-G2M_DEBUG=1 python scripts/e2e_debug.py cl4 > gpurun_out/z_e2e_debug_cl4b.txt 2>&1
-python scripts/e2e_breakdown.py tc > gpurun_out/z_e2e_breakdown_tc.txt 2>&1
-cat gpurun_out/z_e2e_breakdown_cl4.txt gpurun_out/z_e2e_breakdown_tc.txt; grep -v "launch\|class" gpurun_out/z_e2e_debug_cl4b.txt | tail -14
+timeout 600 python -m pytest tests/test_gpu_round2.py -q -x -k "diamond_support or diamond_allreduce or rank_copy or orientation_tiles" > gpurun_out/z_new_tests.log 2>&1; tail -5 gpurun_out/z_new_tests.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+G2M_BENCH_BACKEND=gloo timeout 900 python bench.py --gpus 2 --workload diamond --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/z_bench_diamond_n2gloo.json 2> gpurun_out/z_bench_diamond_n2gloo.err; echo n2 rc=$?; python scripts/line_summary.py gpurun_out/z_bench_diamond_n2gloo.json | cut -c1-300

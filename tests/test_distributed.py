@@ -123,3 +123,66 @@ def test_bench_gpus_mismatch_exits_nonzero():
     out = subprocess.run([sys.executable, str(Path(__file__).resolve().parent.parent / "bench.py"),
                           "--gpus", "2"], capture_output=True, text=True, env=env, timeout=120)
     assert out.returncode == 2 and "WORLD_SIZE" in out.stdout
+
+
+def _support_share(og, chunk, parts, part):
+    """Host restatement of one rank's g2m_diamond_support: triangles whose DAG
+    source u has (u // chunk) % parts == part add 1 to the support of each of
+    their three DAG edges (indexed by oriented slot)."""
+    off = np.asarray(og.row_offsets, dtype=np.int64)
+    nbr = og.neighbors.astype(np.int64)
+    t = np.zeros(len(nbr), dtype=np.int32)
+    slot = {}
+    for u in range(og.num_vertices):
+        for s in range(off[u], off[u + 1]):
+            slot[(u, int(nbr[s]))] = s
+    for u in range(og.num_vertices):
+        if parts > 1 and (u // chunk) % parts != part:
+            continue
+        nu = nbr[off[u]:off[u + 1]]
+        for i, v in enumerate(nu):
+            for w in nu[i + 1:]:
+                for a, b in ((v, w), (w, v)):
+                    s = slot.get((int(a), int(b)))
+                    if s is not None:   # triangle u, v, w
+                        t[slot[(u, int(v))]] += 1
+                        t[slot[(u, int(w))]] += 1
+                        t[s] += 1
+    return t
+
+
+def _support_worker(rank, world, port, results):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = GR.from_edges(G.rmat_edges(9, 8, 5), num_vertices=1 << 9)
+        og = orient_host(g)
+        t = torch.from_numpy(_support_share(og, 4, world, rank))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)            # the one data-path collective
+        n = len(t)
+        mine = t[rank * n // world:(rank + 1) * n // world].to(torch.int64)
+        share = int((mine * (mine - 1) // 2).sum())
+        results[rank] = (D.allreduce_counts({"diamond": share}), t.numpy().tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_diamond_support_allreduce():
+    """The multi-GPU diamond protocol (distributed.diamond_count) with the
+    kernels restated on the host: support shares by source, all-reduce of the
+    support array, C(t, 2) over slot shares, count reduction; equals the
+    oracle's diamond count and the unsplit support."""
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_support_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    g = GR.from_edges(G.rmat_edges(9, 8, 5), num_vertices=1 << 9)
+    want = O.run(g, PL.as_forest(make_plan(diamond(), g, rewrite=True)))[0]
+    full = _support_share(orient_host(g), 4, 1, 0).tolist()
+    for r in range(world):
+        counts, t = results[r]
+        assert counts == want
+        assert t == full

@@ -391,3 +391,67 @@ def test_device_orientation_tiles_equal_host():
         og = pm.orient(g)
         ho = orient_host(g)
         assert og == ho and og.oriented
+
+
+def _support_share(g, rr, device=0):
+    """One rank's support array (torch int32 on the device) and slot count."""
+    import ctypes as C
+    import torch
+    from paper_2112_09761_b200 import _native as N
+    dg = g.device_graph(device)
+    n = C.c_uint64(0)
+    N.check(N.lib().g2m_diamond_support(dg.handle, None, None, C.byref(n), None), "support")
+    t = torch.zeros(max(int(n.value), 1), dtype=torch.int32, device=f"cuda:{device}")
+    spec = EX.source_spec(rr, family="lgs")
+    N.check(N.lib().g2m_diamond_support(dg.handle, C.byref(spec), C.c_void_p(t.data_ptr()), C.byref(n), None),
+            "support")
+    return t, int(n.value)
+
+
+def _choose2(g, t, lo, hi, device=0):
+    import ctypes as C
+    from paper_2112_09761_b200 import _native as N
+    w = np.zeros(2, dtype=np.uint64)
+    N.check(N.lib().g2m_support_choose2(g.device_graph(device).handle, C.c_void_p(t.data_ptr()), lo, hi,
+                                        N.ptr(w, C.c_uint64), None), "choose2")
+    return int(w[0]) | (int(w[1]) << 64)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_diamond_support_split_allreduce_equals_single(parts):
+    """The multi-GPU diamond path with the all-reduce done by hand: the
+    ranks' support arrays (source shares, estimator split) summed, then
+    C(t, 2) over each rank's slot share, add up to the one-device count and
+    to the oracle; and the summed array equals the unsplit support."""
+    import torch
+    from util import diamond
+    g = GR.from_edges(G.rmat_edges(12, 8, 21), num_vertices=1 << 12)
+    want = pm.subgraph_listing(g, diamond(), mode="count").counts["diamond"]
+    full, n = _support_share(g, None)
+    acc = torch.zeros_like(full)
+    for i in range(parts):
+        t, _ = _support_share(g, (256, parts, i) if parts > 1 else None)
+        acc += t
+    torch.cuda.synchronize()
+    assert torch.equal(acc, full)
+    got = sum(_choose2(g, acc, i * n // parts, (i + 1) * n // parts) for i in range(parts))
+    assert got == want
+    f, gg = forest_for_diamond(g)
+    assert want == O.run(gg, f, threads=4)[0]["diamond"]
+
+
+def forest_for_diamond(g):
+    from test_oracle import forest_for
+    return forest_for("diamond", g)
+
+
+def test_bench_multi_rank_diamond_allreduce_gloo():
+    # two ranks folded onto one GPU (gloo): support shares, one all-reduce of
+    # the support array, C(t, 2) per slot share; counts equal the one-rank run
+    common = ["--workload", "diamond", "--scale", "14", "--steps", "2", "--warmup", "1",
+              "--no-cpu-baseline", "--no-e2e", "--no-roofline", "--no-parity"]
+    one = _bench(common)
+    two = _bench(common + ["--gpus", "2"], {"G2M_BENCH_BACKEND": "gloo"})
+    assert one["n_gpus"] == 1 and two["n_gpus"] == 2
+    assert one["counts"] == two["counts"]
+    assert "all-reduce of the per-edge support array" in two["config"]["parallelism"]

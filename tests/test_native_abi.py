@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(N.SIGNATURES)
-    assert lib.g2m_abi_version() == N.ABI_VERSION == 6
+    assert lib.g2m_abi_version() == N.ABI_VERSION == 7
 
 
 def test_struct_layouts():
