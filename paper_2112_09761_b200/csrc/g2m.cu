@@ -548,13 +548,25 @@ __global__ void k_orient_offsets(const u64* off, u64 nv, const u32* keep, const 
 }
 
 // ordered compaction of the kept slots (a warp per keep word)
-__global__ void k_orient_fill_slots(const u32* nbr, u64 slots, const u32* keep, const u64* wpre, u32* out) {
+__global__ void k_orient_fill_slots(const u32* __restrict__ nbr, u64 slots, const u32* __restrict__ keep,
+                                    const u64* __restrict__ wpre, u32* __restrict__ out) {
     const u32 lane = g2m_lane();
     const u64 words = (slots + 31) >> 5;
-    for (u64 w = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; w < words;
-         w += ((u64)gridDim.x * blockDim.x) >> 5) {
-        const u32 m = __ldg(keep + w);
-        if ((m >> lane) & 1u) out[wpre[w] + __popc(m & g2m_lanemask_lt())] = __ldg(nbr + (w << 5) + lane);
+    const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
+    constexpr int B = 4;   // keep words per warp in flight
+    for (u64 w0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; w0 < words; w0 += B * nw) {
+        u32 m[B], x[B];
+        u64 base[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            const u64 w = w0 + q * nw;
+            m[q] = w < words ? __ldg(keep + w) : 0u;
+            base[q] = w < words ? __ldg(wpre + w) : 0ull;
+            x[q] = ((m[q] >> lane) & 1u) ? __ldg(nbr + (w << 5) + lane) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < B; ++q)
+            if ((m[q] >> lane) & 1u) out[base[q] + __popc(m[q] & g2m_lanemask_lt())] = x[q];
     }
 }
 
