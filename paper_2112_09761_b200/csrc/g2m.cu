@@ -1094,11 +1094,11 @@ k_rank_keys64_hubs(const u64* off, const u32* nbr, const u32* rank, int rb, u64*
 // ---- rank-space rows (replaces the global key sort) -------------------------
 // Row r = rank[v] of the rank-space CSR holds rank[w] for w in N(v), sorted.
 // Short rows inside a slot tile are placed by counting (k_rank_fill_tiles),
-// rows up to 1024 slots sorted in a warp's registers (k_rank_fill_warp*),
+// rows up to 512 slots sorted in a warp's registers (k_rank_fill_warp*),
 // longer ones by one 256-thread CTA per row in shared memory (<=
 // kRowSortBlock); graphs with longer rows take the global key sort. RMAT-22
 // (32 M slots): 4.1 ms with a warp walking 32 rows of up to 1024 slots, 2.2 ms
-// with rows > 128 on CTAs, 1.98 ms now (tiles 0.76, warps 0.44 + 0.24 + 0.38).
+// with rows > 128 on CTAs, 1.9 ms now (tiles 0.75, warps 0.44 + 0.24, CTAs).
 constexpr u32 kRowSortBlock = 8192;
 
 // Bitonic sort of s[0, P) (P a power of two) by `nt` threads with index t;
@@ -1287,7 +1287,7 @@ k_rank_fill_warp(const u64* __restrict__ off, const u32* __restrict__ nbr, const
 }
 
 // Listed rows of 32 * E / 2 < d <= 32 * E, a warp each (the register file
-// holds the row: E = 16, 32).
+// holds the row: E = 16).
 template <int E>
 __global__ void __launch_bounds__(128)
 k_rank_fill_warp_big(const u64* __restrict__ off, const u32* __restrict__ nbr, const u32* __restrict__ rank,
@@ -1427,13 +1427,14 @@ static int ensure_rank(const g2m_graph* cg, DevState* st) {
         const u32* rk = rank.as<u32>();
         const u64* ro = g->rk_off.as<u64>();
         u32* rn = g->rk_nbr.as<u32>();
-        st->launches += 5;
+        st->launches += 4;
         k_rank_fill_tiles<<<(int)std::min<u64>(tiles, (u64)st->sms * 7), kTileThreads, 0, st->stream>>>(
             o, nb, nv, slots, rk, ro, rn);
         k_rank_fill_warp<<<st->sms * 8, 256, 0, st->stream>>>(o, nb, rk, ro, rn, wrows);
         k_rank_fill_warp_big<16><<<st->sms * 4, 128, 0, st->stream>>>(o, nb, rk, ro, rn, crows);
-        k_rank_fill_warp_big<32><<<st->sms * 4, 128, 0, st->stream>>>(o, nb, rk, ro, rn, crows);
-        k_rank_fill_hubs<<<st->sms * 6, kRankFillThreads, 0, st->stream>>>(o, nb, rk, ro, rn, crows, 1024u);
+        // rows > 512: one CTA each (a warp with 32 values per lane measured 0.06 ms
+        // slower at RMAT-22: 165 registers, 12 % warps active, i-cache misses)
+        k_rank_fill_hubs<<<st->sms * 6, kRankFillThreads, 0, st->stream>>>(o, nb, rk, ro, rn, crows, 512u);
         G2M_CUDA(cudaGetLastError());
     } else if (nv && slots) {
         int rb = 1;
