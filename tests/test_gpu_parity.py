@@ -391,7 +391,7 @@ def test_instrumented_bytes_match_oracle_rmat11(workload):
     assert EX.algorithmic_bytes(gd, forest) == want
 
 
-def _heavy_source_graph(na=1100):
+def _heavy_source_graph(na=1100, p=0.02):
     """A source u with out-degree na (1100: the W=32/64 tiers; 2100: beyond
     them, the generic fallback for k > 3): u links to A (na vertices); each a
     in A gets na+1 private leaves so deg(a) > deg(u); A is internally an ER
@@ -400,7 +400,7 @@ def _heavy_source_graph(na=1100):
     leaves = na + 1
     A = np.arange(1, na + 1)
     edges = [np.column_stack([np.zeros(na, dtype=np.int64), A])]
-    mask = np.triu(rng.random((na, na)) < 0.02, 1)
+    mask = np.triu(rng.random((na, na)) < p, 1)
     ii, jj = np.nonzero(mask)
     edges.append(np.column_stack([A[ii], A[jj]]))
     base = na + 1
@@ -434,6 +434,20 @@ def test_lgs_clique_kernels_match_generic_and_oracle(k):
     big = complete(1200)      # out-degrees 0..1199: every tier incl. W=32/64
     for kk in (3, 4, 5):
         assert list(pm.k_clique(big, kk).counts.values()) == [comb(1200, kk)]
+
+
+@pytest.mark.parametrize("k", [4, 5])
+def test_lgs_global_slab_tier_medium_density(k):
+    """A source with out-degree 1100 (the global-slab W = 32 tier) whose local
+    graph is ER p = 0.3: rows of ~330 members, k = 5 pairs both light and
+    heavy (> 32 common members); bitmap LGS = plan kernel."""
+    g = _heavy_source_graph(1100, 0.3)
+    og = GR.orient(g)
+    f = PL.as_forest(make_plan(P.generate_clique(k), g, oriented=True))
+    tasks = EX._default_tasks(og, f)
+    a, _, _, _ = EX.execute(og, f, tasks, lgs=True)
+    b, _, _, _ = EX.execute(og, f, tasks, lgs=False)
+    assert a == b
 
 
 def test_rmat12_lgs_known_counts():
