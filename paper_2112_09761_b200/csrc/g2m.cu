@@ -259,6 +259,11 @@ struct g2m_graph {
     // vertex (the orientation's key), so the rank order needs no in-degree pass
     DevBuf symdeg;
     uint64_t symdeg_max = 0;
+    // symmetric graphs uploaded by g2m_graph_create: the orientation's degree
+    // table and keep bits (+ per-word counts), computed on a side stream as
+    // the neighbour chunks land (under the PCIe copy)
+    DevBuf pre_deg, pre_keep, pre_wcnt;
+    bool pre_ready = false;
     uint64_t rk_deg1 = 0;    // ranks [0, rk_deg1) have degree <= 1
     // oriented graphs: rank-space rows holding a column <= their row, i.e. DAG
     // edges against the (degree, id) order (an input oriented some other way)
@@ -333,6 +338,8 @@ extern "C" int g2m_device_count(int32_t* out) {
     return G2M_OK;
 }
 
+static int upload_symmetric_pipelined(g2m_graph* g, DevState* st, const uint64_t* off_h, const uint32_t* nbr_h);
+
 extern "C" int g2m_graph_create(int32_t device, const uint64_t* row_offsets, uint64_t num_vertices,
                                 const uint32_t* neighbors, uint64_t num_slots,
                                 const uint32_t* labels, int32_t oriented, g2m_graph** out) {
@@ -349,12 +356,19 @@ extern "C" int g2m_graph_create(int32_t device, const uint64_t* row_offsets, uin
     g->oriented = oriented ? 1 : 0;
     G2M_TRY(g->off.ensure((num_vertices + 1) * 8));
     G2M_TRY(g->nbr.ensure(std::max<uint64_t>(num_slots, 1) * 4));
-    if (row_offsets)
-        G2M_CUDA(cudaMemcpyAsync(g->off.p, row_offsets, (num_vertices + 1) * 8, cudaMemcpyHostToDevice, st->stream));
-    else
-        G2M_CUDA(cudaMemsetAsync(g->off.p, 0, 8, st->stream));
-    if (num_slots)
-        G2M_CUDA(cudaMemcpyAsync(g->nbr.p, neighbors, num_slots * 4, cudaMemcpyHostToDevice, st->stream));
+    const bool pipe = !oriented && num_vertices && num_slots && row_offsets &&
+                      !(getenv("G2M_UPLOAD_PIPE") && atoi(getenv("G2M_UPLOAD_PIPE")) == 0);
+    if (pipe) {
+        G2M_TRY(upload_symmetric_pipelined(g.get(), st, row_offsets, neighbors));
+    } else {
+        if (row_offsets)
+            G2M_CUDA(cudaMemcpyAsync(g->off.p, row_offsets, (num_vertices + 1) * 8, cudaMemcpyHostToDevice,
+                                     st->stream));
+        else
+            G2M_CUDA(cudaMemsetAsync(g->off.p, 0, 8, st->stream));
+        if (num_slots)
+            G2M_CUDA(cudaMemcpyAsync(g->nbr.p, neighbors, num_slots * 4, cudaMemcpyHostToDevice, st->stream));
+    }
     if (labels) {
         G2M_TRY(g->labels.ensure(std::max<uint64_t>(num_vertices, 1) * 4));
         if (num_vertices)
@@ -513,12 +527,13 @@ __device__ __forceinline__ void tile_rowmap(const u64* off, u64 nv, u64 S0, u64 
 // keep bit of every slot of a symmetric CSR (word s >> 5 = slots 32w ..),
 // and the word's popcount
 __global__ void __launch_bounds__(kTileThreads)
-k_orient_keep_tiles(const u64* off, const u32* nbr, const u32* deg, u64 nv, u64 slots, u32* keep, u64* wcnt) {
+k_orient_keep_tiles(const u64* off, const u32* nbr, const u32* deg, u64 nv, u64 slots, u32* keep, u64* wcnt,
+                    u64 tile0, u64 tile1) {
     __shared__ u32 map[kTileSlots];
     __shared__ u32 scr[kTileThreads / 32];
     __shared__ u64 s_r[2];
     const u32 lane = g2m_lane();
-    for (u64 tile = blockIdx.x; tile * kTileSlots < slots; tile += gridDim.x) {
+    for (u64 tile = tile0 + blockIdx.x; tile < tile1 && tile * kTileSlots < slots; tile += gridDim.x) {
         const u64 S0 = tile * kTileSlots, S1 = min(S0 + kTileSlots, slots);
         tile_rowmap(off, nv, S0, S1, map, scr, s_r);
         for (u32 p = threadIdx.x; p < kTileSlots; p += kTileThreads) {
@@ -570,6 +585,46 @@ __global__ void k_orient_fill_slots(const u32* __restrict__ nbr, u64 slots, cons
     }
 }
 
+// Upload of a symmetric CSR with the orientation's first pass under the copy:
+// the offsets first, then the neighbours in up to 8 tile-aligned chunks on
+// the main stream; a side stream computes the degree table once the offsets
+// are in, then the keep bits of each chunk's tiles as it lands (rows may
+// span chunks: a tile only reads its own slots, and the offsets are all in).
+static int upload_symmetric_pipelined(g2m_graph* g, DevState* st, const uint64_t* off_h, const uint32_t* nbr_h) {
+    const u64 nv = g->nv, slots = g->slots;
+    const u64 words = (slots + 31) >> 5, tiles = (slots + kTileSlots - 1) / kTileSlots;
+    G2M_TRY(g->pre_deg.ensure(std::max<u64>(nv, 1) * 4));
+    G2M_TRY(g->pre_keep.ensure(std::max<u64>(words, 1) * 4));
+    G2M_TRY(g->pre_wcnt.ensure(std::max<u64>(words, 1) * 8));
+    cudaStream_t cs = st->side[0];
+    const u64 per = std::max<u64>((tiles + 7) / 8, 1);
+    const int nchunks = (int)((tiles + per - 1) / per);
+    std::vector<cudaEvent_t> ev(nchunks + 2, nullptr);
+    for (auto& e : ev) G2M_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    G2M_CUDA(cudaMemcpyAsync(g->off.p, off_h, (nv + 1) * 8, cudaMemcpyHostToDevice, st->stream));
+    G2M_CUDA(cudaEventRecord(ev[0], st->stream));
+    G2M_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+    ++st->launches;
+    k_degrees<<<grid_for(st, nv, 256), 256, 0, cs>>>(g->off.as<u64>(), nv, g->pre_deg.as<u32>());
+    for (int c = 0; c < nchunks; ++c) {
+        const u64 t0 = (u64)c * per, t1 = std::min<u64>(tiles, t0 + per);
+        const u64 a = t0 * kTileSlots, b = std::min<u64>(slots, t1 * kTileSlots);
+        G2M_CUDA(cudaMemcpyAsync(g->nbr.as<u32>() + a, nbr_h + a, (b - a) * 4, cudaMemcpyHostToDevice, st->stream));
+        G2M_CUDA(cudaEventRecord(ev[1 + c], st->stream));
+        G2M_CUDA(cudaStreamWaitEvent(cs, ev[1 + c], 0));
+        ++st->launches;
+        k_orient_keep_tiles<<<(int)std::min<u64>(t1 - t0, (u64)st->sms * 8), kTileThreads, 0, cs>>>(
+            g->off.as<u64>(), g->nbr.as<u32>(), g->pre_deg.as<u32>(), nv, slots, g->pre_keep.as<u32>(),
+            g->pre_wcnt.as<u64>(), t0, t1);
+    }
+    G2M_CUDA(cudaGetLastError());
+    G2M_CUDA(cudaEventRecord(ev[nchunks + 1], cs));
+    G2M_CUDA(cudaStreamWaitEvent(st->stream, ev[nchunks + 1], 0));
+    for (auto& e : ev) cudaEventDestroy(e);   // released once the recorded work completes
+    g->pre_ready = true;
+    return G2M_OK;
+}
+
 static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     auto o = std::make_unique<g2m_graph>();
     o->dev = g->dev;
@@ -591,26 +646,38 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     // offsets from the prefix at each row start, an ordered compaction
     // (RMAT-22: 1.1 ms, against 2.5 ms for warp-per-row count and fill passes)
     const u64 words = (g->slots + 31) >> 5;
-    DevBuf keep;
-    G2M_TRY(keep.ensure(std::max<u64>(words, 1) * 4));
-    G2M_TRY(st->tmp1.ensure(std::max<u64>(words, 1) * 8));
+    DevBuf keepbuf;
     G2M_TRY(st->tmp3.ensure((words + 1) * 8));
-    u64* wcnt = st->tmp1.as<u64>();
     u64* wpre = st->tmp3.as<u64>();
-    ++st->launches;
-    k_degrees<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, deg.as<u32>());
-    if (g->slots) {
+    const u32* keep;
+    const u64* wcnt;
+    if (g->pre_ready) {   // computed under the upload (upload_symmetric_pipelined)
+        G2M_CUDA(cudaMemcpyAsync(deg.p, g->pre_deg.p, std::max<u64>(g->nv, 1) * 4, cudaMemcpyDeviceToDevice,
+                                 st->stream));
+        keep = g->pre_keep.as<u32>();
+        wcnt = g->pre_wcnt.as<u64>();
+    } else {
+        G2M_TRY(keepbuf.ensure(std::max<u64>(words, 1) * 4));
+        G2M_TRY(st->tmp1.ensure(std::max<u64>(words, 1) * 8));
+        u64* wc = st->tmp1.as<u64>();
         ++st->launches;
-        const u64 tiles = (g->slots + kTileSlots - 1) / kTileSlots;
-        k_orient_keep_tiles<<<(int)std::min<u64>(tiles, (u64)st->sms * 8), kTileThreads, 0, st->stream>>>(
-            g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv, g->slots, keep.as<u32>(), wcnt);
+        k_degrees<<<grid_for(st, g->nv, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, deg.as<u32>());
+        if (g->slots) {
+            ++st->launches;
+            const u64 tiles = (g->slots + kTileSlots - 1) / kTileSlots;
+            k_orient_keep_tiles<<<(int)std::min<u64>(tiles, (u64)st->sms * 8), kTileThreads, 0, st->stream>>>(
+                g->off.as<u64>(), g->nbr.as<u32>(), deg.as<u32>(), g->nv, g->slots, keepbuf.as<u32>(), wc, 0,
+                tiles);
+        }
+        keep = keepbuf.as<u32>();
+        wcnt = wc;
     }
     G2M_CUDA(cudaGetLastError());
     phase("degrees+keep");
     G2M_TRY(exclusive_scan_u64(st, wcnt, wpre, words));
     ++st->launches;
-    k_orient_offsets<<<grid_for(st, g->nv + 1, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, keep.as<u32>(),
-                                                                            wpre, o->off.as<u64>());
+    k_orient_offsets<<<grid_for(st, g->nv + 1, 256), 256, 0, st->stream>>>(g->off.as<u64>(), g->nv, keep, wpre,
+                                                                            o->off.as<u64>());
     G2M_CUDA(cudaGetLastError());
     G2M_CUDA(cudaMemcpyAsync(&o->slots, o->off.as<u64>() + g->nv, 8, cudaMemcpyDeviceToHost, st->stream));
     G2M_CUDA(cudaStreamSynchronize(st->stream));
@@ -619,7 +686,7 @@ static int orient_impl(const g2m_graph* g, DevState* st, g2m_graph** out) {
     if (words) {
         ++st->launches;
         k_orient_fill_slots<<<grid_for(st, words * 32, 256), 256, 0, st->stream>>>(
-            g->nbr.as<u32>(), g->slots, keep.as<u32>(), wpre, o->nbr.as<u32>());
+            g->nbr.as<u32>(), g->slots, keep, wpre, o->nbr.as<u32>());
         G2M_CUDA(cudaGetLastError());
     }
     if (g->labels.p) {
